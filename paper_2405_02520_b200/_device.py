@@ -1,0 +1,61 @@
+"""Device-buffer plumbing: numpy/torch inputs -> contiguous CUDA tensors.
+
+Device (torch CUDA) inputs stay on the device and results are returned as
+CUDA tensors. Host inputs (numpy arrays, CPU tensors, lists) are the
+drop-in path of the reference's numpy API: they are staged through pinned
+memory, transformed on the GPU and returned as numpy arrays of the plan's
+dtype. Nothing is computed on the host.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+_TORCH = {np.dtype(np.complex64): torch.complex64, np.dtype(np.complex128): torch.complex128}
+_NUMPY = {torch.complex64: np.complex64, torch.complex128: np.complex128}
+
+
+def require_cuda():
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2405_02520_b200 needs a CUDA device (there is no CPU fallback)")
+
+
+def torch_dtype(np_dtype):
+    return _TORCH[np.dtype(np_dtype)]
+
+
+def is_device(x) -> bool:
+    return isinstance(x, torch.Tensor) and x.is_cuda
+
+
+def to_device(x, np_dtype, device=None):
+    """Return (contiguous CUDA tensor of the plan dtype, input_was_host)."""
+    require_cuda()
+    td = torch_dtype(np_dtype)
+    if isinstance(x, torch.Tensor):
+        if x.is_cuda:
+            t = x if x.dtype == td else x.to(td)
+            return t.contiguous(), False
+        host = x.to(td).contiguous()
+    else:
+        arr = np.ascontiguousarray(np.asarray(x), dtype=np_dtype)
+        host = torch.from_numpy(arr)
+    dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+    if host.numel() * host.element_size() >= (1 << 20):
+        if not host.is_pinned():
+            host = host.pin_memory()
+        return host.to(dev, non_blocking=True), True
+    return host.to(dev), True
+
+
+def to_host(t: torch.Tensor) -> np.ndarray:
+    return t.cpu().numpy()
+
+
+def stream_ptr():
+    return torch.cuda.current_stream().cuda_stream
+
+
+def ptr(t) -> int | None:
+    return None if t is None else t.data_ptr()

@@ -1,0 +1,323 @@
+// Multi-launch tiled FFT for N > 2^13 (reference stages 2-3,
+// fft_core/execute.py:82-106 and planner.py:82-97), with the ABFT checksums
+// carried across launches as per-tile partial sums.
+//
+// Every launch is one "pass" = one reference stage: a batch of L-point
+// transforms (L = stage dim) addressed through
+//     in (u, j) = hi*in_hi  + lo*in_lo  + j*in_j       u = hi*lo_count + lo
+//     out(u, k) = hi*out_hi + lo*out_lo + k*out_k
+// A CTA owns U consecutive transforms u (a "tile") of one signal, lanes run
+// along u, so every global row segment is U*sizeof(complex) contiguous bytes.
+//   kind 0 (first stage): strided columns c of the (d0 x rest) view, post
+//          twiddle w_N^{c k}; stores back in place (no transpose copy — the
+//          reference's ascontiguousarray transposes disappear into the
+//          address maps); accumulates c_in = x.(e^T W) and the l1 mass per
+//          tile from the pristine input;
+//   kind 1 (3-stage middle): columns c2 inside each k0 block, twiddle
+//          w_{d1 d2}^{c2 k};
+//   kind 2 (last stage): contiguous rows staged through shared memory,
+//          stores an (N1 x N3) plane per CTA — consecutive k0 lanes write
+//          consecutive output addresses f = k0 + d0*(k1 + d1*k) — and
+//          accumulates c_out = y.e per tile.
+// A finalize kernel reduces the tile partials per signal in a fixed order and
+// takes the detection decision (reference abft/pipeline.py:104-135).
+#pragma once
+#include "single.cuh"
+
+namespace tfft {
+
+enum { KIND_FIRST = 0, KIND_MID = 1, KIND_LAST = 2 };
+
+template <class T>
+struct PassArgs {
+    const C<T>* in;
+    C<T>* out;
+    long long batch, sig_base, n;
+    long long lo_count, in_hi, in_lo, in_j, out_hi, out_lo, out_k;
+    long long tiles_per_sig;          // units / U
+    const C<T>* twL;                  // w_L^k, k < L
+    const C<T>* ptw_lo;               // post twiddle w_M^e = hi[e >> s] * lo[e & mask]
+    const C<T>* ptw_hi;
+    int ptw_shift;
+    long long ptw_mask, M;            // M - 1 == mask for e reduction
+    const C<T>* etw;                  // kind 0 ABFT row
+    const C<T>* values;               // kind 2 table encoding
+    T* part;                          // tile partials (3 or 2 T per tile)
+    int inverse, scale_inv;
+    T scale;
+    long long f_signal, f_unit;
+    int f_idx, f_where, f_comp, f_bit;  // f_where: 1 after load, 2 store pre-scale, 3 post-scale
+};
+
+template <class T>
+__device__ __forceinline__ T block_reduce_sum(T v, T* sh, int nwarps) {
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) v = fadd(v, shfl_xor(v, off));
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+    __syncthreads();
+    T s = T(0);
+    if (threadIdx.x == 0) {
+        s = sh[0];
+        for (int w = 1; w < nwarps; ++w) s = fadd(s, sh[w]);
+    }
+    return s;
+}
+
+template <class T, int L, int E, int U, int P, int KIND, int ABFT, class Radices>
+__global__ void __launch_bounds__(U * (L / E))
+fft_pass_kernel(const PassArgs<T> a) {
+    constexpr int TPS = L / E;
+    constexpr int THREADS = U * TPS;
+    constexpr int RS = U + P;  // smem row stride (elements) of the [L][U] tile
+    using Eng = Engine<T, L, E, Radices>;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    C<T>* tile = reinterpret_cast<C<T>*>(smem_raw);
+    T* red = reinterpret_cast<T*>(tile + L * RS);
+
+    const int u = threadIdx.x % U;
+    const int t = threadIdx.x / U;
+    const long long total = a.batch * a.tiles_per_sig;
+
+    struct Mem {
+        C<T>* base;
+        int u;
+        __device__ __forceinline__ void put(int i, C<T> v) const { base[i * RS + u] = v; }
+        __device__ __forceinline__ C<T> get(int i) const { return base[i * RS + u]; }
+        __device__ __forceinline__ void sync() const { __syncthreads(); }
+    };
+    const Mem mem{tile, u};
+
+    for (long long tix = blockIdx.x; tix < total; tix += gridDim.x) {
+        const long long b = tix / a.tiles_per_sig;
+        const long long tsig = tix - b * a.tiles_per_sig;
+        const long long u0 = tsig * U;               // first unit of the tile
+        const long long uu = u0 + u;
+        const long long hi = uu / a.lo_count, lo = uu - hi * a.lo_count;
+        const C<T>* src = a.in + b * a.n;
+        C<T>* dst = a.out + b * a.n;
+        const long long ibase = hi * a.in_hi + lo * a.in_lo;
+        const long long obase = hi * a.out_hi + lo * a.out_lo;
+        const bool fsig = a.f_where != 0 && (a.sig_base + b) == a.f_signal && uu == a.f_unit &&
+                          (a.f_idx % TPS) == t;
+        const int fm = a.f_idx / TPS;
+
+        C<T> v[E];
+        if constexpr (KIND == KIND_LAST) {
+            // rows are contiguous: stage the U x L tile through smem with
+            // j-fastest (fully coalesced) loads.
+            const long long hi0 = u0 / a.lo_count, lo0 = u0 - hi0 * a.lo_count;
+            const long long rbase0 = hi0 * a.in_hi + lo0 * a.in_lo;
+#pragma unroll 4
+            for (int f = threadIdx.x; f < U * L; f += THREADS) {
+                const int r = f / L, j = f % L;
+                tile[j * RS + r] = __ldcs(src + rbase0 + (long long)r * a.in_lo + j);
+            }
+            __syncthreads();
+#pragma unroll
+            for (int m = 0; m < E; ++m) v[m] = tile[(t + m * TPS) * RS + u];
+            __syncthreads();
+        } else {
+#pragma unroll
+            for (int m = 0; m < E; ++m) v[m] = __ldcs(src + ibase + (long long)(t + m * TPS) * a.in_j);
+        }
+
+        if constexpr (KIND == KIND_FIRST && ABFT != ABFT_OFF) {
+            C<T> cin = mk<T>(T(0), T(0));
+            T l1 = T(0);
+#pragma unroll
+            for (int m = 0; m < E; ++m) {
+                const C<T> e = __ldg(a.etw + ibase + (long long)(t + m * TPS) * a.in_j);
+                cin.x = ffma(v[m].x, e.x, ffma(-v[m].y, e.y, cin.x));
+                cin.y = ffma(v[m].x, e.y, ffma(v[m].y, e.x, cin.y));
+                l1 = fadd(l1, mag_fast(v[m]));
+            }
+            T s0 = block_reduce_sum(cin.x, red, THREADS / 32);
+            T s1 = block_reduce_sum(cin.y, red, THREADS / 32);
+            T s2 = block_reduce_sum(l1, red, THREADS / 32);
+            if (threadIdx.x == 0) {
+                T* p = a.part + tix * 3;
+                p[0] = s0; p[1] = s1; p[2] = s2;
+            }
+        }
+        if (fsig && a.f_where == 1) {
+#pragma unroll
+            for (int m = 0; m < E; ++m) if (m == fm) flip_component<T>(v[m], a.f_comp, a.f_bit);
+        }
+
+        if (a.inverse) {
+#pragma unroll
+            for (int m = 0; m < E; ++m) v[m] = swapri<T>(v[m]);
+        }
+        Eng::run(v, mem, t, a.twL);
+        if constexpr (KIND != KIND_LAST) {
+            // post twiddle w_M^{c k} with c = lo (column), k = t + m*TPS
+#pragma unroll
+            for (int m = 0; m < E; ++m) {
+                const long long e = (lo * (long long)(t + m * TPS)) & a.ptw_mask;
+                const C<T> w = cmul<T>(__ldg(a.ptw_hi + (e >> a.ptw_shift)),
+                                       __ldg(a.ptw_lo + (e & ((1ll << a.ptw_shift) - 1))));
+                v[m] = cmul<T>(v[m], w);
+            }
+        }
+        if (a.inverse) {
+#pragma unroll
+            for (int m = 0; m < E; ++m) v[m] = swapri<T>(v[m]);
+        }
+        if (fsig && a.f_where == 2) {
+#pragma unroll
+            for (int m = 0; m < E; ++m) if (m == fm) flip_component<T>(v[m], a.f_comp, a.f_bit);
+        }
+        if constexpr (KIND == KIND_LAST) {
+            if (a.scale_inv) {
+#pragma unroll
+                for (int m = 0; m < E; ++m) v[m] = cscale<T>(v[m], a.scale);
+            }
+            if (fsig && a.f_where == 3) {
+#pragma unroll
+                for (int m = 0; m < E; ++m) if (m == fm) flip_component<T>(v[m], a.f_comp, a.f_bit);
+            }
+        }
+#pragma unroll
+        for (int m = 0; m < E; ++m) __stcs(dst + obase + (long long)(t + m * TPS) * a.out_k, v[m]);
+
+        if constexpr (KIND == KIND_LAST && ABFT != ABFT_OFF) {
+            C<T> cout = mk<T>(T(0), T(0));
+            const T hr = T(-0.5), hq = T(0.8660254037844386467637232);
+#pragma unroll
+            for (int m = 0; m < E; ++m) {
+                const long long f = obase + (long long)(t + m * TPS) * a.out_k;
+                C<T> e;
+                if constexpr (ABFT == ABFT_TABLE) {
+                    e = __ldg(a.values + f);
+                } else {
+                    const int cls = (int)(f % 3);
+                    e = cls == 0 ? mk<T>(T(1), T(0)) : (cls == 1 ? mk<T>(hr, -hq) : mk<T>(hr, hq));
+                }
+                cout = cadd<T>(cout, cmul<T>(v[m], e));
+            }
+            T s0 = block_reduce_sum(cout.x, red, THREADS / 32);
+            T s1 = block_reduce_sum(cout.y, red, THREADS / 32);
+            if (threadIdx.x == 0) {
+                T* p = a.part + tix * 2;
+                p[0] = s0; p[1] = s1;
+            }
+        }
+        __syncthreads();  // smem tile reused by the next iteration
+    }
+}
+
+// Per-signal reduction of the tile partials and the detection decision.
+template <class T>
+struct FinalArgs {
+    long long batch, sig_base;
+    const T* part_in;  long long tiles_in;
+    const T* part_out; long long tiles_out;
+    T delta, abs_floor, floor_coef;
+    int* flag_count;
+    long long* flag_sig;
+    T* flag_rel;
+    long long flag_cap;
+    typename KeyT<T>::type* max_key;
+};
+
+template <class T>
+__global__ void __launch_bounds__(256) abft_finalize_kernel(const FinalArgs<T> a) {
+    __shared__ typename KeyT<T>::type cta_max;
+    if (threadIdx.x == 0) cta_max = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const long long warps = (long long)gridDim.x * (blockDim.x / 32);
+    T my_max = T(0);
+    for (long long b = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); b < a.batch; b += warps) {
+        T ci_x = 0, ci_y = 0, l1 = 0, co_x = 0, co_y = 0;
+        for (long long i = lane; i < a.tiles_in; i += 32) {
+            const T* p = a.part_in + (b * a.tiles_in + i) * 3;
+            ci_x = fadd(ci_x, p[0]); ci_y = fadd(ci_y, p[1]); l1 = fadd(l1, p[2]);
+        }
+        for (long long i = lane; i < a.tiles_out; i += 32) {
+            const T* p = a.part_out + (b * a.tiles_out + i) * 2;
+            co_x = fadd(co_x, p[0]); co_y = fadd(co_y, p[1]);
+        }
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) {
+            ci_x = fadd(ci_x, shfl_xor(ci_x, off)); ci_y = fadd(ci_y, shfl_xor(ci_y, off));
+            l1 = fadd(l1, shfl_xor(l1, off));
+            co_x = fadd(co_x, shfl_xor(co_x, off)); co_y = fadd(co_y, shfl_xor(co_y, off));
+        }
+        if (lane == 0) {
+            const C<T> raw = mk<T>(fsub(ci_x, co_x), fsub(ci_y, co_y));
+            const T fl = nanmax<T>(a.abs_floor, fmul(a.floor_coef, l1));
+            const T den = nanmax<T>(cabs<T>(mk<T>(ci_x, ci_y)), fl);
+            T rel = cabs<T>(raw) / den;
+            if (!isfinite(rel)) rel = T(INFINITY);
+            my_max = my_max > rel ? my_max : rel;
+            if (rel > a.delta) {
+                const int slot = atomicAdd(a.flag_count, 1);
+                if (slot < a.flag_cap) {
+                    a.flag_sig[slot] = a.sig_base + b;
+                    a.flag_rel[slot] = rel;
+                }
+            }
+        }
+    }
+    if (lane == 0 && my_max > T(0)) atomicMax(&cta_max, order_key(my_max));
+    __syncthreads();
+    if (threadIdx.x == 0 && cta_max) atomicMax(a.max_key, cta_max);
+}
+
+// ------------------------------------------------------------------ host
+struct PassEntry {
+    int logl;
+    int e, u, p, threads, smem;
+    const void* fn[3][3];  // [kind][abft]
+};
+extern const PassEntry kPass_fp32[];
+extern const int kPassCount_fp32;
+extern const PassEntry kPass_fp64[];
+extern const int kPassCount_fp64;
+
+struct MultiPlan {
+    int prec = 0;
+    int nst = 0;
+    long long n = 0;
+    long long d[3] = {0, 0, 0};
+    int num_sms = 148;
+    const PassEntry* pe[3] = {nullptr, nullptr, nullptr};
+    void* twL[3] = {nullptr, nullptr, nullptr};        // w_{d_k}^i tables
+    void* ptw_lo[2] = {nullptr, nullptr};              // post twiddles per non-last stage
+    void* ptw_hi[2] = {nullptr, nullptr};
+    int ptw_shift[2] = {0, 0};
+    void* ws = nullptr;                                // intermediate batch buffer
+    size_t ws_bytes = 0;
+    void* part = nullptr;                              // ABFT partials
+    size_t part_bytes = 0;
+};
+
+struct MultiLaunch {
+    const void* in;
+    void* out;
+    long long batch, sig_base;
+    int inverse, scale_inv, abft;
+    const void* etw;
+    const void* values;
+    double delta, abs_floor;
+    long long f_signal, f_elem;
+    int f_where, f_stage, f_comp, f_bit;
+    int* flag_count;
+    long long* flag_sig;
+    void* flag_rel;
+    long long flag_cap;
+    unsigned long long* max_key;
+    int only_stage;  // -1: whole transform; k: just stage k, in -> out
+};
+
+int multi_plan_init(MultiPlan& mp, long long n, int prec, int nst, const int64_t* dims, int num_sms);
+int multi_launch(MultiPlan& mp, const MultiLaunch& m, cudaStream_t st);
+// Only stage `k` (no ABFT, no scaling): in -> out in the pass layout.
+int multi_launch_stage(MultiPlan& mp, int k, const void* in, void* out, long long batch, int inverse,
+                       cudaStream_t st);
+void multi_plan_free(MultiPlan& mp);
+const char* multi_last_error();
+
+}  // namespace tfft

@@ -1,0 +1,334 @@
+// Host side of the multi-launch path: twiddle tables, workspace and the
+// per-stage launch sequence (reference fft_core/execute.py:82-106 — each
+// reference stage is one launch here; the transposes become address maps).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/tfft.h"
+#include "multi.cuh"
+
+namespace tfft {
+
+namespace {
+thread_local std::string m_err;
+int merr(int code, const std::string& s) {
+    m_err = s;
+    return code;
+}
+#define MCU(call)                                                                            \
+    do {                                                                                     \
+        cudaError_t e_ = (call);                                                             \
+        if (e_ != cudaSuccess) return merr(TFFT_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+int lg(long long n) {
+    int l = 0;
+    while ((1ll << l) < n) ++l;
+    return l;
+}
+
+// exp(-2 pi i k / N) with quadrant symmetry (long double).
+void root(long long N, long long k, long double* re, long double* im) {
+    k %= N;
+    if (k < 0) k += N;
+    const long double two_pi = 6.283185307179586476925286766559005768L;
+    long double c, s;
+    if ((4 * k) % N == 0) {
+        const int q = (int)((4 * k) / N);
+        c = q == 0 ? 1.0L : (q == 2 ? -1.0L : 0.0L);
+        s = q == 1 ? 1.0L : (q == 3 ? -1.0L : 0.0L);
+    } else {
+        const long long qn = N / 4;
+        const int q = (int)(k / qn);
+        const long long r = k - q * qn;
+        long double c1, s1;
+        if (2 * r <= qn) {
+            c1 = cosl(two_pi * (long double)r / (long double)N);
+            s1 = sinl(two_pi * (long double)r / (long double)N);
+        } else {
+            c1 = sinl(two_pi * (long double)(qn - r) / (long double)N);
+            s1 = cosl(two_pi * (long double)(qn - r) / (long double)N);
+        }
+        switch (q) {
+            case 0: c = c1; s = s1; break;
+            case 1: c = -s1; s = c1; break;
+            case 2: c = -c1; s = -s1; break;
+            default: c = s1; s = -c1; break;
+        }
+    }
+    *re = c;
+    *im = -s;
+}
+
+int upload_roots(int prec, long long N, long long count, long long stride, void** dst) {
+    const size_t es = prec == TFFT_FP32 ? 8 : 16;
+    MCU(cudaMalloc(dst, count * es));
+    std::vector<unsigned char> h(count * es);
+    for (long long k = 0; k < count; ++k) {
+        long double re, im;
+        root(N, k * stride, &re, &im);
+        if (prec == TFFT_FP32) {
+            float2 v = make_float2((float)re, (float)im);
+            memcpy(&h[k * es], &v, es);
+        } else {
+            double2 v = make_double2((double)re, (double)im);
+            memcpy(&h[k * es], &v, es);
+        }
+    }
+    MCU(cudaMemcpy(*dst, h.data(), count * es, cudaMemcpyHostToDevice));
+    return TFFT_OK;
+}
+
+const PassEntry* pass_entry(int prec, int logl) {
+    const PassEntry* tab = prec == TFFT_FP32 ? kPass_fp32 : kPass_fp64;
+    const int cnt = prec == TFFT_FP32 ? kPassCount_fp32 : kPassCount_fp64;
+    for (int i = 0; i < cnt; ++i)
+        if (tab[i].logl == logl) return &tab[i];
+    return nullptr;
+}
+
+std::mutex occ_mu;
+std::map<const void*, int> occ;
+
+int blocks_per_sm(const void* fn, int threads, int smem, int* nb) {
+    std::lock_guard<std::mutex> lk(occ_mu);
+    auto it = occ.find(fn);
+    if (it != occ.end()) {
+        *nb = it->second;
+        return TFFT_OK;
+    }
+    if (smem > 48 * 1024) MCU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    int v = 0;
+    MCU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, fn, threads, smem));
+    if (v < 1) return merr(TFFT_EUNSUPPORTED, "pass kernel does not fit on an SM");
+    occ[fn] = v;
+    *nb = v;
+    return TFFT_OK;
+}
+
+template <class T>
+int launch_pass(const MultiPlan& mp, const PassEntry* pe, int kind, int abft, PassArgs<T>& a, int num_sms,
+                cudaStream_t st) {
+    const void* fn = pe->fn[kind][abft];
+    if (!fn) return merr(TFFT_EUNSUPPORTED, "pass variant not built");
+    int nb = 0;
+    int rc = blocks_per_sm(fn, pe->threads, pe->smem, &nb);
+    if (rc) return rc;
+    const long long total = a.batch * a.tiles_per_sig;
+    long long grid = std::min<long long>(total, (long long)nb * num_sms);
+    if (grid < 1) grid = 1;
+    void* args[] = {&a};
+    MCU(cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(pe->threads), args, pe->smem, st));
+    return TFFT_OK;
+}
+
+template <class T>
+int multi_launch_t(MultiPlan& mp, const MultiLaunch& m, cudaStream_t st) {
+    const long long n = mp.n;
+    const int nst = mp.nst;
+    const long long d0 = mp.d[0], d1 = mp.d[1], d2 = mp.d[2];
+    const long long R0 = n / d0;
+    const size_t es = sizeof(C<T>);
+    const size_t need = m.only_stage >= 0 ? 0 : (size_t)m.batch * n * es;
+    if (need > mp.ws_bytes) {
+        cudaFree(mp.ws);
+        mp.ws = nullptr;
+        mp.ws_bytes = 0;
+        MCU(cudaMalloc(&mp.ws, need));
+        mp.ws_bytes = need;
+    }
+    const bool abft = m.abft != ABFT_OFF;
+    long long tiles[3];
+    for (int k = 0; k < nst; ++k) {
+        const long long units = k == 0 ? R0 : (k == nst - 1 ? n / mp.d[k] : d0 * d2);
+        tiles[k] = units / mp.pe[k]->u;
+    }
+    T* part_in = nullptr;
+    T* part_out = nullptr;
+    if (abft) {
+        const size_t pb = (size_t)m.batch * (tiles[0] * 3 + tiles[nst - 1] * 2) * sizeof(T);
+        if (pb > mp.part_bytes) {
+            cudaFree(mp.part);
+            mp.part = nullptr;
+            mp.part_bytes = 0;
+            MCU(cudaMalloc(&mp.part, pb));
+            mp.part_bytes = pb;
+        }
+        part_in = (T*)mp.part;
+        part_out = part_in + (size_t)m.batch * tiles[0] * 3;
+    }
+
+    for (int k = 0; k < nst; ++k) {
+        if (m.only_stage >= 0 && k != m.only_stage) continue;
+        const int kind = k == 0 ? KIND_FIRST : (k == nst - 1 ? KIND_LAST : KIND_MID);
+        PassArgs<T> a;
+        memset(&a, 0, sizeof(a));
+        a.batch = m.batch;
+        a.sig_base = m.sig_base;
+        a.n = n;
+        a.in = (const C<T>*)(k == 0 || m.only_stage >= 0 ? m.in : mp.ws);
+        a.out = (C<T>*)(k == nst - 1 || m.only_stage >= 0 ? m.out : mp.ws);
+        a.tiles_per_sig = tiles[k];
+        a.twL = (const C<T>*)mp.twL[k];
+        a.inverse = m.inverse;
+        a.scale_inv = m.scale_inv;
+        a.scale = T(1) / T(n);
+        if (kind == KIND_FIRST) {
+            a.lo_count = R0; a.in_hi = 0; a.in_lo = 1; a.in_j = R0;
+            a.out_hi = 0; a.out_lo = 1; a.out_k = R0;
+            a.M = n;
+        } else if (kind == KIND_MID) {
+            a.lo_count = d2; a.in_hi = R0; a.in_lo = 1; a.in_j = d2;
+            a.out_hi = R0; a.out_lo = 1; a.out_k = d2;
+            a.M = d1 * d2;
+        } else if (nst == 2) {
+            a.lo_count = d0; a.in_hi = 0; a.in_lo = R0; a.in_j = 1;
+            a.out_hi = 0; a.out_lo = 1; a.out_k = d0;
+        } else {
+            a.lo_count = d0; a.in_hi = d2; a.in_lo = R0; a.in_j = 1;
+            a.out_hi = d0; a.out_lo = 1; a.out_k = d0 * d1;
+        }
+        if (kind != KIND_LAST) {
+            a.ptw_lo = (const C<T>*)mp.ptw_lo[k];
+            a.ptw_hi = (const C<T>*)mp.ptw_hi[k];
+            a.ptw_shift = mp.ptw_shift[k];
+            a.ptw_mask = a.M - 1;
+        }
+        int abft_v = ABFT_OFF;
+        if (abft && kind == KIND_FIRST) {
+            abft_v = ABFT_WANG;  // input side: table row, any encoding
+            a.etw = (const C<T>*)m.etw;
+            a.part = part_in;
+        } else if (abft && kind == KIND_LAST) {
+            abft_v = m.abft;
+            a.values = (const C<T>*)m.values;
+            a.part = part_out;
+        }
+        // fault for this pass
+        if (m.f_where != 0) {
+            const long long e = m.f_elem;
+            a.f_signal = m.f_signal;
+            a.f_comp = m.f_comp;
+            a.f_bit = m.f_bit;
+            if (m.f_where == 1 && k == 0) {                 // input: x[j*R0 + c]
+                a.f_where = 1; a.f_unit = e % R0; a.f_idx = (int)(e / R0);
+            } else if (m.f_where == 2 && m.f_stage == k) {  // stage:k, reference layout
+                a.f_where = 2;
+                if (k == 0) {                                // c*d0 + k0
+                    a.f_unit = e / d0; a.f_idx = (int)(e % d0);
+                } else if (kind == KIND_MID) {               // (k0*d2 + c2)*d1 + k1
+                    a.f_unit = e / d1; a.f_idx = (int)(e % d1);
+                } else if (nst == 2) {                       // k0*d1 + k1
+                    a.f_unit = e / d1; a.f_idx = (int)(e % d1);
+                } else {                                     // (k0*d1 + k1)*d2 + k2
+                    const long long k0 = e / (d1 * d2), k1 = (e / d2) % d1;
+                    a.f_unit = k1 * d0 + k0; a.f_idx = (int)(e % d2);
+                }
+            } else if (m.f_where == 3 && kind == KIND_LAST) {  // natural output index f
+                a.f_where = 3;
+                if (nst == 2) {
+                    a.f_unit = e % d0; a.f_idx = (int)(e / d0);
+                } else {
+                    const long long k0 = e % d0, k1 = (e / d0) % d1;
+                    a.f_unit = k1 * d0 + k0; a.f_idx = (int)(e / (d0 * d1));
+                }
+            }
+        }
+        int rc = launch_pass<T>(mp, mp.pe[k], kind, abft_v, a, mp.num_sms, st);
+        if (rc) return rc;
+    }
+    if (abft) {
+        FinalArgs<T> f;
+        memset(&f, 0, sizeof(f));
+        f.batch = m.batch;
+        f.sig_base = m.sig_base;
+        f.part_in = part_in;
+        f.tiles_in = tiles[0];
+        f.part_out = part_out;
+        f.tiles_out = tiles[nst - 1];
+        f.delta = (T)m.delta;
+        f.abs_floor = (T)m.abs_floor;
+        f.floor_coef = sizeof(T) == 4 ? (T)1e-6f : (T)1e-12;
+        f.flag_count = m.flag_count;
+        f.flag_sig = m.flag_sig;
+        f.flag_rel = (T*)m.flag_rel;
+        f.flag_cap = m.flag_cap;
+        f.max_key = (typename KeyT<T>::type*)m.max_key;
+        const long long grid = std::min<long long>((m.batch + 7) / 8, 4LL * mp.num_sms);
+        abft_finalize_kernel<T><<<(unsigned)std::max<long long>(grid, 1), 256, 0, st>>>(f);
+        MCU(cudaGetLastError());
+    }
+    return TFFT_OK;
+}
+
+}  // namespace
+
+const char* multi_last_error() { return m_err.c_str(); }
+
+int multi_plan_init(MultiPlan& mp, long long n, int prec, int nst, const int64_t* dims, int num_sms) {
+    mp.prec = prec;
+    mp.nst = nst;
+    mp.n = n;
+    mp.num_sms = num_sms;
+    if (nst < 2) return merr(TFFT_EUNSUPPORTED, "multi-pass plan needs >= 2 stages");
+    for (int k = 0; k < nst; ++k) mp.d[k] = dims[k];
+    const long long R0 = n / mp.d[0];
+    for (int k = 0; k < nst; ++k) {
+        mp.pe[k] = pass_entry(prec, lg(mp.d[k]));
+        if (!mp.pe[k]) return merr(TFFT_EUNSUPPORTED, "no pass kernel for stage dim");
+        const int kind = k == 0 ? KIND_FIRST : (k == nst - 1 ? KIND_LAST : KIND_MID);
+        const long long lo_count = kind == KIND_FIRST ? R0 : (kind == KIND_MID ? mp.d[2] : mp.d[0]);
+        if (lo_count % mp.pe[k]->u) return merr(TFFT_EUNSUPPORTED, "stage split too narrow for the tile width");
+        int rc = upload_roots(prec, mp.d[k], mp.d[k], 1, &mp.twL[k]);
+        if (rc) return rc;
+        if (kind != KIND_LAST) {
+            const long long M = kind == KIND_FIRST ? n : mp.d[1] * mp.d[2];
+            const int lm = lg(M);
+            const int s = (lm + 1) / 2;
+            mp.ptw_shift[k] = s;
+            rc = upload_roots(prec, M, 1ll << s, 1, &mp.ptw_lo[k]);
+            if (rc) return rc;
+            rc = upload_roots(prec, M, M >> s, 1ll << s, &mp.ptw_hi[k]);
+            if (rc) return rc;
+        }
+    }
+    return TFFT_OK;
+}
+
+void multi_plan_free(MultiPlan& mp) {
+    for (int k = 0; k < 3; ++k) { cudaFree(mp.twL[k]); mp.twL[k] = nullptr; }
+    for (int k = 0; k < 2; ++k) {
+        cudaFree(mp.ptw_lo[k]); cudaFree(mp.ptw_hi[k]);
+        mp.ptw_lo[k] = mp.ptw_hi[k] = nullptr;
+    }
+    cudaFree(mp.ws); mp.ws = nullptr; mp.ws_bytes = 0;
+    cudaFree(mp.part); mp.part = nullptr; mp.part_bytes = 0;
+}
+
+int multi_launch_stage(MultiPlan& mp, int k, const void* in, void* out, long long batch, int inverse,
+                       cudaStream_t st) {
+    if (k < 0 || k >= mp.nst) return merr(TFFT_EINVAL, "stage index out of range");
+    MultiLaunch m;
+    memset(&m, 0, sizeof(m));
+    m.in = in;
+    m.out = out;
+    m.batch = batch;
+    m.inverse = inverse;
+    m.abft = ABFT_OFF;
+    m.only_stage = k;
+    return multi_launch(mp, m, st);
+}
+
+int multi_launch(MultiPlan& mp, const MultiLaunch& m, cudaStream_t st) {
+    if (m.batch == 0) return TFFT_OK;
+    return mp.prec == TFFT_FP32 ? multi_launch_t<float>(mp, m, st) : multi_launch_t<double>(mp, m, st);
+}
+
+}  // namespace tfft

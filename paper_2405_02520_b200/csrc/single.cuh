@@ -1,0 +1,247 @@
+// Single-kernel fault-tolerant FFT for N <= 2^13 (one reference "stage",
+// reference planner.py:20-23), with two-sided ABFT fused into its only memory
+// pass:
+//   load   : x -> registers; left-side input checksum c_in = x . (e^T W) and the
+//            l1 mass are accumulated from the pristine values (reference
+//            abft/pipeline.py:72-85, protected.py:105-109);
+//   compute: Stockham passes in registers + padded smem (engine.cuh);
+//   store  : y -> HBM; output checksum c_out = y . e (Wang weights folded
+//            into three residue-class sums), per-signal relative discrepancy
+//            and the flag decision (pipeline.py:104-135) are computed while the
+//            results are stored. Only flagged signals and the running max are
+//            written — no per-signal HBM traffic on the fault-free path.
+// The cross-batch (right-side) combination s0 = sum_b x_b is rebuilt from the
+// preserved input only for flagged groups ("s0").
+#pragma once
+#include "engine.cuh"
+
+namespace tfft {
+
+enum { AT_NONE = 0, AT_INPUT = 1, AT_PRESCALE = 2, AT_OUTPUT = 3 };
+enum { ABFT_OFF = 0, ABFT_WANG = 1, ABFT_TABLE = 2 };
+
+template <class T> struct KeyT;
+template <> struct KeyT<float>  { using type = unsigned int; };
+template <> struct KeyT<double> { using type = unsigned long long; };
+
+template <class T>
+struct SingleArgs {
+    const C<T>* in;
+    C<T>* out;
+    long long batch;        // signals in this launch
+    long long sig_base;     // global index of signal 0 (for reports)
+    const C<T>* tw;         // w_N^k, k < N
+    const C<T>* etw;        // input-side checksum row (e^T W or e^T W^-1), plan dtype
+    const C<T>* values;     // encoding weights (ABFT_TABLE only)
+    T delta, abs_floor, floor_coef;
+    int inverse;            // conjugate-direction transform
+    int scale_inv;          // multiply by 1/N (fft_execute inverse; tile_fft never)
+    // results
+    int* flag_count;
+    long long* flag_sig;
+    T* flag_rel;
+    long long flag_cap;
+    typename KeyT<T>::type* max_key;
+    T* rel_out;             // optional per-signal relative discrepancy
+    // one device-side fault (reference fault_lab/bits.py:56-77 semantics)
+    long long f_signal, f_elem;
+    int f_where, f_comp, f_bit;
+};
+
+template <class T> __device__ __forceinline__ T nanmax(T a, T b) {
+    return (a != a) ? a : ((b != b) ? b : (a > b ? a : b));
+}
+
+// Sum `val` over the TPS consecutive threads of one signal (deterministic
+// tree). For TPS > 32 the per-warp partials go through `scratch` (one slot
+// per warp of the CTA); only thread t == 0 of the signal gets the total.
+template <int TPS, class T>
+__device__ __forceinline__ T sig_sum(T val, T* scratch, int t) {
+    constexpr int W = TPS < 32 ? TPS : 32;
+#pragma unroll
+    for (int off = W / 2; off >= 1; off >>= 1) val = fadd(val, shfl_xor(val, off));
+    if constexpr (TPS > 32) {
+        const int warp = threadIdx.x >> 5;
+        __syncthreads();
+        if ((threadIdx.x & 31) == 0) scratch[warp] = val;
+        __syncthreads();
+        if (t == 0) {
+            T s = scratch[warp];
+#pragma unroll
+            for (int w = 1; w < TPS / 32; ++w) s = fadd(s, scratch[warp + w]);
+            val = s;
+        }
+    }
+    return val;
+}
+
+template <class T, int N, int E, int PS, int ABFT, int THREADS, class Radices>
+__global__ void __launch_bounds__(THREADS)
+fft_single_kernel(const SingleArgs<T> a) {
+    using Eng = Engine<T, N, E, Radices>;
+    constexpr int TPS = N / E;
+    constexpr int S = THREADS / TPS;  // signals per CTA
+    static_assert(S >= 1 && S * TPS == THREADS, "CTA must hold whole signals");
+    constexpr bool MULTIPASS = RCount<Radices>::v > 1;
+    constexpr int SLEN = MULTIPASS ? SmemLen<N, PS>::v : 0;
+    constexpr int NW = THREADS / 32 > 0 ? THREADS / 32 : 1;
+
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    C<T>* sm_all = reinterpret_cast<C<T>*>(smem_raw);
+    T* red = reinterpret_cast<T*>(sm_all + S * SLEN);  // NW partial sums
+    __shared__ typename KeyT<T>::type cta_max;
+
+    const int sl = threadIdx.x / TPS;
+    const int t = threadIdx.x % TPS;
+    C<T>* sm = sm_all + sl * SLEN;
+    T my_max = T(0);
+    if (threadIdx.x == 0) cta_max = 0;
+
+    const long long tiles = (a.batch + S - 1) / S;
+    for (long long tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+        const long long b = tile * S + sl;
+        const bool live = b < a.batch;
+        const C<T>* src = a.in + b * N;
+        C<T>* dst = a.out + b * N;
+
+        C<T> v[E];
+        if (live) {
+#pragma unroll
+            for (int m = 0; m < E; ++m) {
+                if constexpr (TPS >= 4) v[m] = __ldcs(src + t + m * TPS);
+                else v[m] = src[t + m * TPS];
+            }
+        } else {
+#pragma unroll
+            for (int m = 0; m < E; ++m) v[m] = mk<T>(T(0), T(0));
+        }
+
+        // ---- left-side input checksum on the pristine values
+        C<T> cin = mk<T>(T(0), T(0));
+        T l1 = T(0);
+        if constexpr (ABFT != ABFT_OFF) {
+#pragma unroll
+            for (int m = 0; m < E; ++m) {
+                const C<T> e = __ldg(a.etw + t + m * TPS);
+                cin.x = ffma(v[m].x, e.x, ffma(-v[m].y, e.y, cin.x));
+                cin.y = ffma(v[m].x, e.y, ffma(v[m].y, e.x, cin.y));
+                l1 = fadd(l1, mag_fast(v[m]));
+            }
+        }
+        const bool fault_here = a.f_where != AT_NONE && live && (a.sig_base + b) == a.f_signal &&
+                                (int)(a.f_elem % TPS) == t;
+        const int fm = (int)(a.f_elem / TPS);
+        if (fault_here && a.f_where == AT_INPUT) {
+#pragma unroll
+            for (int m = 0; m < E; ++m) if (m == fm) flip_component<T>(v[m], a.f_comp, a.f_bit);
+        }
+
+        // ---- transform (inverse = swap(FFT(swap(x))) — conjugate symmetry)
+        if (a.inverse) {
+#pragma unroll
+            for (int m = 0; m < E; ++m) v[m] = swapri<T>(v[m]);
+        }
+        Eng::run(v, SliceMem<T, TPS, PS>{sm}, t, a.tw);
+        if (a.inverse) {
+#pragma unroll
+            for (int m = 0; m < E; ++m) v[m] = swapri<T>(v[m]);
+        }
+        if (fault_here && a.f_where == AT_PRESCALE) {
+#pragma unroll
+            for (int m = 0; m < E; ++m) if (m == fm) flip_component<T>(v[m], a.f_comp, a.f_bit);
+        }
+        if (a.scale_inv) {
+            const T s = T(1) / T(N);  // exact power of two
+#pragma unroll
+            for (int m = 0; m < E; ++m) v[m] = cscale<T>(v[m], s);
+        }
+        if (fault_here && a.f_where == AT_OUTPUT) {
+#pragma unroll
+            for (int m = 0; m < E; ++m) if (m == fm) flip_component<T>(v[m], a.f_comp, a.f_bit);
+        }
+
+        // ---- store + output checksum
+        if (live) {
+#pragma unroll
+            for (int m = 0; m < E; ++m) {
+                if constexpr (TPS >= 4) __stcs(dst + t + m * TPS, v[m]);
+                else dst[t + m * TPS] = v[m];
+            }
+        }
+        if constexpr (ABFT != ABFT_OFF) {
+            C<T> cout = mk<T>(T(0), T(0));
+            if constexpr (ABFT == ABFT_WANG) {
+                // e_k = w3^(k mod 3): sum per residue class, then 3 weights.
+                C<T> acc[3] = {mk<T>(T(0), T(0)), mk<T>(T(0), T(0)), mk<T>(T(0), T(0))};
+#pragma unroll
+                for (int m = 0; m < E; ++m) acc[m % 3] = cadd<T>(acc[m % 3], v[m]);
+                constexpr int tau = TPS % 3;  // 1 or 2 (TPS is a power of two)
+                const int t0 = t % 3;
+                constexpr T hr = T(-0.5), hi = T(0.8660254037844386467637232);
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    if (c >= E) break;
+                    const int cls = (t0 + c * tau) % 3;
+                    const T wy = cls == 0 ? T(0) : (cls == 1 ? -hi : hi);
+                    const T wx = cls == 0 ? T(1) : hr;
+                    cout = cadd<T>(cout, cmul<T>(acc[c], mk<T>(wx, wy)));
+                }
+            } else {
+#pragma unroll
+                for (int m = 0; m < E; ++m) {
+                    const C<T> e = __ldg(a.values + t + m * TPS);
+                    cout = cadd<T>(cout, cmul<T>(v[m], e));
+                }
+            }
+            T r0 = sig_sum<TPS>(cin.x, red, t);
+            T r1 = sig_sum<TPS>(cin.y, red, t);
+            T r2 = sig_sum<TPS>(cout.x, red, t);
+            T r3 = sig_sum<TPS>(cout.y, red, t);
+            T r4 = sig_sum<TPS>(l1, red, t);
+            bool flagged = false;
+            T rel = T(0);
+            if (t == 0 && live) {
+                const C<T> cI = mk<T>(r0, r1);
+                const C<T> raw = mk<T>(fsub(r0, r2), fsub(r1, r3));
+                const T fl = nanmax<T>(a.abs_floor, fmul(a.floor_coef, r4));
+                const T den = nanmax<T>(cabs<T>(cI), fl);
+                rel = cabs<T>(raw) / den;
+                if (!isfinite(rel)) rel = T(INFINITY);
+                flagged = rel > a.delta;
+                my_max = my_max > rel ? my_max : rel;
+                if (a.rel_out) a.rel_out[b] = rel;
+            }
+            // warp-aggregated append of flagged signals (rare)
+            const unsigned ball = __ballot_sync(0xffffffffu, flagged);
+            if (ball) {
+                const int lane = threadIdx.x & 31;
+                int base = 0;
+                if (lane == __ffs(ball) - 1) base = atomicAdd(a.flag_count, __popc(ball));
+                base = __shfl_sync(0xffffffffu, base, __ffs(ball) - 1);
+                if (flagged) {
+                    const long long slot = base + __popc(ball & ((1u << lane) - 1u));
+                    if (slot < a.flag_cap) {
+                        a.flag_sig[slot] = a.sig_base + b;
+                        a.flag_rel[slot] = rel;
+                    }
+                }
+            }
+        }
+    }
+    if constexpr (ABFT != ABFT_OFF) {
+        // one atomic per CTA for the running max discrepancy
+        typename KeyT<T>::type k = order_key(my_max);
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) {
+            typename KeyT<T>::type o = __shfl_xor_sync(0xffffffffu, k, off);
+            k = o > k ? o : k;
+        }
+        __syncthreads();
+        if ((threadIdx.x & 31) == 0 && k) atomicMax(&cta_max, k);
+        __syncthreads();
+        if (threadIdx.x == 0 && cta_max) atomicMax(a.max_key, cta_max);
+    }
+    (void)NW;
+}
+
+}  // namespace tfft

@@ -1,0 +1,774 @@
+// C ABI (include/tfft.h) of the B200 fault-tolerant FFT: plan objects,
+// launch dispatch and the run_protected orchestration
+// (reference abft/protected.py:63-166).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/tfft.h"
+#include "aux_kernels.cuh"
+#include "multi.cuh"
+#include "registry.h"
+
+using namespace tfft;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+#define CU(call)                                                                   \
+    do {                                                                           \
+        cudaError_t e_ = (call);                                                   \
+        if (e_ != cudaSuccess)                                                     \
+            return fail(TFFT_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+int ilog2(int64_t n) {
+    int l = 0;
+    while ((int64_t(1) << l) < n) ++l;
+    return l;
+}
+bool is_pow2(int64_t n) { return n >= 1 && (n & (n - 1)) == 0; }
+
+// exp(-2*pi*i*k/N) in long double with exact axis values and quadrant symmetry.
+void unit_root(int64_t N, int64_t k, long double* re, long double* im) {
+    k %= N;
+    if (k < 0) k += N;
+    const long double two_pi = 6.283185307179586476925286766559005768L;
+    long double c, s;  // cos, sin of 2*pi*k/N
+    if ((4 * k) % N == 0) {
+        const int q = (int)((4 * k) / N);
+        c = q == 0 ? 1.0L : (q == 2 ? -1.0L : 0.0L);
+        s = q == 1 ? 1.0L : (q == 3 ? -1.0L : 0.0L);
+    } else {
+        const int64_t qn = N / 4;  // N >= 8 here
+        const int q = (int)(k / qn);
+        const int64_t r = k - q * qn;  // 0 < r < N/4
+        long double c1, s1;
+        if (2 * r <= qn) {
+            c1 = cosl(two_pi * (long double)r / (long double)N);
+            s1 = sinl(two_pi * (long double)r / (long double)N);
+        } else {
+            c1 = sinl(two_pi * (long double)(qn - r) / (long double)N);
+            s1 = cosl(two_pi * (long double)(qn - r) / (long double)N);
+        }
+        switch (q) {
+            case 0: c = c1; s = s1; break;
+            case 1: c = -s1; s = c1; break;
+            case 2: c = -c1; s = -s1; break;
+            default: c = s1; s = -c1; break;
+        }
+    }
+    *re = c;
+    *im = -s;
+}
+
+template <class T>
+std::vector<C<T>> root_table(int64_t N, int64_t count, int64_t stride) {
+    std::vector<C<T>> t(count);
+    for (int64_t k = 0; k < count; ++k) {
+        long double re, im;
+        unit_root(N, k * stride, &re, &im);
+        t[k].x = (T)re;
+        t[k].y = (T)im;
+    }
+    return t;
+}
+
+struct Counters {
+    int flag_count;
+    int pad;
+    unsigned long long max_key;  // float key in low 32 bits for fp32
+};
+
+const SingleEntry* single_entry(int prec, int logn) {
+    const SingleEntry* tab = prec == TFFT_FP32 ? kSingle_fp32 : kSingle_fp64;
+    const int cnt = prec == TFFT_FP32 ? kSingleCount_fp32 : kSingleCount_fp64;
+    for (int i = 0; i < cnt; ++i)
+        if (tab[i].logn == logn) return &tab[i];
+    return nullptr;
+}
+
+std::mutex g_attr_mu;
+std::map<const void*, int> g_blocks_per_sm;
+
+int prepare_kernel(const void* fn, int threads, int smem, int* blocks_per_sm) {
+    std::lock_guard<std::mutex> lk(g_attr_mu);
+    auto it = g_blocks_per_sm.find(fn);
+    if (it != g_blocks_per_sm.end()) {
+        *blocks_per_sm = it->second;
+        return TFFT_OK;
+    }
+    if (smem > 48 * 1024) CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    int nb = 0;
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, threads, smem));
+    if (nb < 1) return fail(TFFT_EUNSUPPORTED, "kernel does not fit on an SM");
+    g_blocks_per_sm[fn] = nb;
+    *blocks_per_sm = nb;
+    return TFFT_OK;
+}
+
+}  // namespace
+
+struct tfft_plan {
+    int64_t n = 0;
+    int prec = 0;
+    int nstages = 0;
+    int64_t dims[3] = {0, 0, 0};
+    int64_t bs = 1;
+    int device = 0;
+    int logn = 0;
+    int num_sms = 148;
+    size_t esize = 8;               // bytes per complex element
+    // single-kernel path
+    const SingleEntry* single = nullptr;
+    void* tw = nullptr;             // w_N^k, k < N (single-kernel path)
+    // multi-pass path
+    MultiPlan multi;
+    // workspace
+    Counters* d_cnt = nullptr;
+    Counters* h_cnt = nullptr;      // pinned
+    long long* d_flag_sig = nullptr;
+    void* d_flag_rel = nullptr;
+    int64_t flag_cap = 0;
+    void* d_scratch = nullptr;      // correction staging
+    size_t scratch_bytes = 0;
+    FixJob* d_jobs = nullptr;
+    int64_t jobs_cap = 0;
+    cudaEvent_t ev_done = nullptr;  // detection summary landed in h_cnt
+};
+
+namespace {
+
+int ensure_flags(tfft_plan* p, int64_t batch) {
+    if (batch <= p->flag_cap) return TFFT_OK;
+    cudaFree(p->d_flag_sig);
+    cudaFree(p->d_flag_rel);
+    p->d_flag_sig = nullptr;
+    p->d_flag_rel = nullptr;
+    CU(cudaMalloc(&p->d_flag_sig, batch * sizeof(long long)));
+    CU(cudaMalloc(&p->d_flag_rel, batch * sizeof(double)));
+    p->flag_cap = batch;
+    return TFFT_OK;
+}
+
+int ensure_scratch(tfft_plan* p, size_t bytes) {
+    if (bytes <= p->scratch_bytes) return TFFT_OK;
+    cudaFree(p->d_scratch);
+    p->d_scratch = nullptr;
+    CU(cudaMalloc(&p->d_scratch, bytes));
+    p->scratch_bytes = bytes;
+    return TFFT_OK;
+}
+
+// Per-launch transform description shared by every path.
+struct Launch {
+    const void* in;
+    void* out;
+    int64_t batch;
+    int64_t sig_base;
+    int inverse;
+    int scale_inv;
+    int abft;              // ABFT_OFF / ABFT_WANG / ABFT_TABLE
+    const void* etw;
+    const void* values;
+    double delta, abs_floor;
+    // fault translated for this launch
+    long long f_signal, f_elem;
+    int f_where, f_stage, f_comp, f_bit;
+};
+
+template <class T>
+int launch_single_t(tfft_plan* p, const Launch& L, cudaStream_t st) {
+    const SingleEntry* e = p->single;
+    const void* fn = e->fn[L.abft];
+    int nb = 0;
+    int rc = prepare_kernel(fn, e->threads, e->smem, &nb);
+    if (rc) return rc;
+    SingleArgs<T> a;
+    memset(&a, 0, sizeof(a));
+    a.in = (const C<T>*)L.in;
+    a.out = (C<T>*)L.out;
+    a.batch = L.batch;
+    a.sig_base = L.sig_base;
+    a.tw = (const C<T>*)p->tw;
+    a.etw = (const C<T>*)L.etw;
+    a.values = (const C<T>*)L.values;
+    a.delta = (T)L.delta;
+    a.abs_floor = (T)L.abs_floor;
+    a.floor_coef = p->prec == TFFT_FP32 ? (T)1e-6f : (T)1e-12;
+    a.inverse = L.inverse;
+    a.scale_inv = L.scale_inv;
+    a.flag_count = &p->d_cnt->flag_count;
+    a.flag_sig = p->d_flag_sig;
+    a.flag_rel = (T*)p->d_flag_rel;
+    a.flag_cap = p->flag_cap;
+    a.max_key = (typename KeyT<T>::type*)&p->d_cnt->max_key;
+    a.rel_out = nullptr;
+    a.f_signal = L.f_signal;
+    a.f_elem = L.f_elem;
+    a.f_where = L.f_where;
+    a.f_comp = L.f_comp;
+    a.f_bit = L.f_bit;
+    const int S = e->threads / e->tps;
+    const long long tiles = (L.batch + S - 1) / S;
+    long long grid = std::min<long long>(tiles, (long long)nb * p->num_sms);
+    if (grid < 1) grid = 1;
+    void* args[] = {&a};
+    CU(cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(e->threads), args, e->smem, st));
+    return TFFT_OK;
+}
+
+int launch_transform(tfft_plan* p, const Launch& L, cudaStream_t st) {
+    if (L.batch == 0) return TFFT_OK;
+    if (p->single) {
+        return p->prec == TFFT_FP32 ? launch_single_t<float>(p, L, st)
+                                    : launch_single_t<double>(p, L, st);
+    }
+    MultiLaunch m;
+    m.in = L.in; m.out = L.out; m.batch = L.batch; m.sig_base = L.sig_base;
+    m.inverse = L.inverse; m.scale_inv = L.scale_inv; m.abft = L.abft;
+    m.etw = L.etw; m.values = L.values; m.delta = L.delta; m.abs_floor = L.abs_floor;
+    m.f_signal = L.f_signal; m.f_elem = L.f_elem; m.f_where = L.f_where;
+    m.f_stage = L.f_stage; m.f_comp = L.f_comp; m.f_bit = L.f_bit;
+    m.flag_count = &p->d_cnt->flag_count;
+    m.flag_sig = p->d_flag_sig;
+    m.flag_rel = p->d_flag_rel;
+    m.flag_cap = p->flag_cap;
+    m.max_key = &p->d_cnt->max_key;
+    m.only_stage = -1;
+    int rc = multi_launch(p->multi, m, st);
+    if (rc) return fail(rc, multi_last_error());
+    return TFFT_OK;
+}
+
+Launch base_launch(const void* in, void* out, int64_t batch, int inverse) {
+    Launch L;
+    memset(&L, 0, sizeof(L));
+    L.in = in;
+    L.out = out;
+    L.batch = batch;
+    L.inverse = inverse;
+    L.scale_inv = inverse;
+    L.abft = ABFT_OFF;
+    L.f_where = AT_NONE;
+    return L;
+}
+
+int check_plan(tfft_plan* p) {
+    if (!p) return fail(TFFT_EINVAL, "null plan");
+    CU(cudaSetDevice(p->device));
+    return TFFT_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* tfft_last_error(void) { return g_err.c_str(); }
+int tfft_version(void) { return 1; }
+
+int tfft_plan_create(tfft_plan** out, int64_t n, int precision, int nstages, const int64_t* dims,
+                     int64_t bs, int device) {
+    if (!out) return fail(TFFT_EINVAL, "null output handle");
+    *out = nullptr;
+    if (!is_pow2(n) || n < 2) return fail(TFFT_EINVAL, "n must be a power of two >= 2");
+    if (precision != TFFT_FP32 && precision != TFFT_FP64) return fail(TFFT_EINVAL, "bad precision");
+    if (nstages < 1 || nstages > 3 || !dims) return fail(TFFT_EINVAL, "plans use 1 to 3 stages");
+    int64_t prod = 1;
+    for (int i = 0; i < nstages; ++i) {
+        if (!is_pow2(dims[i]) || dims[i] < 2) return fail(TFFT_EINVAL, "stage dims must be powers of two");
+        prod *= dims[i];
+    }
+    if (prod != n) return fail(TFFT_EINVAL, "stage dims must multiply to n");
+    if (bs < 1) return fail(TFFT_EINVAL, "bs must be >= 1");
+    if (n > (int64_t(1) << 25)) return fail(TFFT_EUNSUPPORTED, "n above 2^25 not built");
+    CU(cudaSetDevice(device));
+    tfft_plan* p = new tfft_plan();
+    p->n = n;
+    p->prec = precision;
+    p->nstages = nstages;
+    for (int i = 0; i < nstages; ++i) p->dims[i] = dims[i];
+    p->bs = bs;
+    p->device = device;
+    p->logn = ilog2(n);
+    p->esize = precision == TFFT_FP32 ? 8 : 16;
+    cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, device);
+    int rc = TFFT_OK;
+    auto cleanup = [&](int code) {
+        tfft_plan_destroy(p);
+        return code;
+    };
+    if (p->logn <= 13) {
+        p->single = single_entry(precision, p->logn);
+        if (!p->single) return cleanup(fail(TFFT_EUNSUPPORTED, "no single-kernel config"));
+        size_t bytes = (size_t)n * p->esize;
+        if (cudaMalloc(&p->tw, bytes) != cudaSuccess) return cleanup(fail(TFFT_ENOMEM, "twiddle alloc"));
+        cudaError_t ce;
+        if (precision == TFFT_FP32) {
+            auto t = root_table<float>(n, n, 1);
+            ce = cudaMemcpy(p->tw, t.data(), bytes, cudaMemcpyHostToDevice);
+        } else {
+            auto t = root_table<double>(n, n, 1);
+            ce = cudaMemcpy(p->tw, t.data(), bytes, cudaMemcpyHostToDevice);
+        }
+        if (ce != cudaSuccess) return cleanup(fail(TFFT_ECUDA, cudaGetErrorString(ce)));
+    } else {
+        rc = multi_plan_init(p->multi, n, precision, nstages, dims, p->num_sms);
+        if (rc) return cleanup(fail(rc, multi_last_error()));
+    }
+    if (cudaMalloc(&p->d_cnt, sizeof(Counters)) != cudaSuccess) return cleanup(fail(TFFT_ENOMEM, "counters"));
+    if (cudaMallocHost(&p->h_cnt, sizeof(Counters)) != cudaSuccess) return cleanup(fail(TFFT_ENOMEM, "pinned counters"));
+    *out = p;
+    return TFFT_OK;
+}
+
+int tfft_plan_destroy(tfft_plan* p) {
+    if (!p) return TFFT_OK;
+    cudaSetDevice(p->device);
+    cudaFree(p->tw);
+    multi_plan_free(p->multi);
+    cudaFree(p->d_cnt);
+    cudaFreeHost(p->h_cnt);
+    cudaFree(p->d_flag_sig);
+    cudaFree(p->d_flag_rel);
+    cudaFree(p->d_scratch);
+    cudaFree(p->d_jobs);
+    if (p->ev_done) cudaEventDestroy(p->ev_done);
+    delete p;
+    return TFFT_OK;
+}
+
+int tfft_execute(tfft_plan* p, const void* in, void* out, int64_t batch, int inverse, void* stream) {
+    int rc = check_plan(p);
+    if (rc) return rc;
+    if (batch < 0 || (batch > 0 && (!in || !out))) return fail(TFFT_EINVAL, "bad buffers");
+    Launch L = base_launch(in, out, batch, inverse ? 1 : 0);
+    return launch_transform(p, L, (cudaStream_t)stream);
+}
+
+int tfft_execute_stage(tfft_plan* p, int k, const void* in, void* out, int64_t batch, int inverse,
+                       void* stream) {
+    int rc = check_plan(p);
+    if (rc) return rc;
+    if (batch < 0 || (batch > 0 && (!in || !out))) return fail(TFFT_EINVAL, "bad buffers");
+    if (k < 0 || k >= p->nstages) return fail(TFFT_EINVAL, "stage index out of range");
+    if (batch == 0) return TFFT_OK;
+    if (p->single) {
+        if (p->nstages != 1)
+            return fail(TFFT_EUNSUPPORTED, "per-stage execution of a multi-stage plan needs n > 2^13");
+        Launch L = base_launch(in, out, batch, inverse ? 1 : 0);
+        L.scale_inv = 0;
+        return launch_transform(p, L, (cudaStream_t)stream);
+    }
+    rc = multi_launch_stage(p->multi, k, in, out, batch, inverse ? 1 : 0, (cudaStream_t)stream);
+    if (rc) return fail(rc, multi_last_error());
+    return TFFT_OK;
+}
+
+int tfft_scale(void* buf, int64_t count, int dtype_bytes, double s, void* stream) {
+    if (!buf || count < 0) return fail(TFFT_EINVAL, "bad buffer");
+    if (dtype_bytes != 8 && dtype_bytes != 16) return fail(TFFT_EINVAL, "unsupported dtype");
+    if (count == 0) return TFFT_OK;
+    const int grid = (int)std::min<long long>((count + 255) / 256, 1 << 16);
+    if (dtype_bytes == 8)
+        scale_kernel<float><<<grid, 256, 0, (cudaStream_t)stream>>>((float2*)buf, count, (float)s);
+    else
+        scale_kernel<double><<<grid, 256, 0, (cudaStream_t)stream>>>((double2*)buf, count, s);
+    CU(cudaGetLastError());
+    return TFFT_OK;
+}
+
+int tfft_flip_bit(void* buf, int64_t word, int bit, int dtype_bytes, void* stream) {
+    if (!buf || word < 0) return fail(TFFT_EINVAL, "bad buffer");
+    const int wbytes = dtype_bytes / 2;
+    if (wbytes != 4 && wbytes != 8) return fail(TFFT_EINVAL, "dtype must be complex64/complex128");
+    if (bit < 0 || bit >= wbytes * 8) return fail(TFFT_EINVAL, "bit out of range");
+    flip_word_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(buf, word, bit, wbytes);
+    CU(cudaGetLastError());
+    return TFFT_OK;
+}
+
+int tfft_encode_group(tfft_plan* p, const void* xg, int64_t bs, const void* row, void* s0, void* s1,
+                      void* c_in, void* x_l1, void* stream) {
+    int rc = check_plan(p);
+    if (rc) return rc;
+    if (!xg || bs < 1) return fail(TFFT_EINVAL, "bad group");
+    cudaStream_t st = (cudaStream_t)stream;
+    const long long n = p->n;
+    if (s0 || s1) {
+        int grid = (int)std::min<long long>((n + 255) / 256, 4LL * p->num_sms);
+        if (p->prec == TFFT_FP32)
+            group_sums_kernel<float><<<grid, 256, 0, st>>>((const float2*)xg, bs, n, (float2*)s0, (double2*)s1);
+        else
+            group_sums_kernel<double><<<grid, 256, 0, st>>>((const double2*)xg, bs, n, (double2*)s0, (double2*)s1);
+        CU(cudaGetLastError());
+    }
+    if (c_in || x_l1) {
+        if (p->prec == TFFT_FP32)
+            dot_l1_kernel<float><<<(unsigned)bs, AUX_THREADS, 0, st>>>((const float2*)xg, n, (const float2*)row,
+                                                                       (float2*)c_in, (float*)x_l1);
+        else
+            dot_l1_kernel<double><<<(unsigned)bs, AUX_THREADS, 0, st>>>((const double2*)xg, n, (const double2*)row,
+                                                                        (double2*)c_in, (double*)x_l1);
+        CU(cudaGetLastError());
+    }
+    return TFFT_OK;
+}
+
+int tfft_detect(tfft_plan* p, const void* yg, int64_t bs, const void* values, const void* c_in,
+                const void* x_l1, double abs_floor, void* rel, void* raw, void* stream) {
+    int rc = check_plan(p);
+    if (rc) return rc;
+    if (!yg || !c_in || !x_l1 || !rel || bs < 1) return fail(TFFT_EINVAL, "bad buffers");
+    cudaStream_t st = (cudaStream_t)stream;
+    if (p->prec == TFFT_FP32)
+        detect_kernel<float><<<(unsigned)bs, AUX_THREADS, 0, st>>>(
+            (const float2*)yg, p->n, (const float2*)values, (const float2*)c_in, (const float*)x_l1,
+            (float)abs_floor, 1e-6f, (float*)rel, (float2*)raw);
+    else
+        detect_kernel<double><<<(unsigned)bs, AUX_THREADS, 0, st>>>(
+            (const double2*)yg, p->n, (const double2*)values, (const double2*)c_in, (const double*)x_l1,
+            abs_floor, 1e-12, (double*)rel, (double2*)raw);
+    CU(cudaGetLastError());
+    return TFFT_OK;
+}
+
+int tfft_correct_signal(tfft_plan* p, const void* s0, const void* yg, int64_t bs, int64_t f, void* fixed,
+                        int inverse, void* stream) {
+    int rc = check_plan(p);
+    if (rc) return rc;
+    if (!s0 || !yg || !fixed || f < 0 || f >= bs) return fail(TFFT_EINVAL, "bad arguments");
+    cudaStream_t st = (cudaStream_t)stream;
+    rc = ensure_scratch(p, p->n * p->esize);
+    if (rc) return rc;
+    Launch L = base_launch(s0, p->d_scratch, 1, inverse ? 1 : 0);
+    rc = launch_transform(p, L, st);
+    if (rc) return rc;
+    int grid = (int)std::min<long long>((p->n + 255) / 256, 4LL * p->num_sms);
+    if (p->prec == TFFT_FP32)
+        rebuild_kernel<float><<<grid, 256, 0, st>>>((const float2*)p->d_scratch, (const float2*)yg, bs, p->n, f,
+                                                    (float2*)fixed);
+    else
+        rebuild_kernel<double><<<grid, 256, 0, st>>>((const double2*)p->d_scratch, (const double2*)yg, bs, p->n,
+                                                     f, (double2*)fixed);
+    CU(cudaGetLastError());
+    return TFFT_OK;
+}
+
+int tfft_run_protected(tfft_plan* p, const void* in, void* out, int64_t batch, int scheme, double delta,
+                       double abs_floor, const void* etw, const void* values, const tfft_fault* fault,
+                       int inverse, tfft_report* rep, void* stream) {
+    int rc = tfft_protect_launch(p, in, out, batch, scheme, delta, abs_floor, etw, values, fault, inverse, rep,
+                                 stream);
+    if (rc) return rc;
+    return tfft_protect_finish(p, in, out, batch, scheme, delta, abs_floor, etw, values, inverse, rep, stream);
+}
+
+int tfft_protect_launch(tfft_plan* p, const void* in, void* out, int64_t batch, int scheme, double delta,
+                        double abs_floor, const void* etw, const void* values, const tfft_fault* fault,
+                        int inverse, tfft_report* rep, void* stream) {
+    int rc = check_plan(p);
+    if (rc) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (!rep) return fail(TFFT_EINVAL, "null report");
+    if (batch < 1 || !in || !out) return fail(TFFT_EINVAL, "batch must have shape (B, n) with n == plan.n");
+    if (batch % p->bs) return fail(TFFT_EINVAL, "batch size not divisible by group size");
+    if (scheme < TFFT_SCHEME_NONE || scheme > TFFT_SCHEME_TWO_SIDED_GROUP) return fail(TFFT_EINVAL, "bad scheme");
+    const bool prot = scheme != TFFT_SCHEME_NONE;
+    if (prot && !etw) return fail(TFFT_EINVAL, "protected schemes need the encoding row");
+    if (prot && !(delta > 0)) return fail(TFFT_EINVAL, "delta must be positive");
+    const int64_t groups = batch / p->bs;
+    const int64_t n = p->n;
+    rep->groups = groups;
+    rep->recompute_count = 0;
+    rep->pass_count = 2 * (int64_t)p->nstages * groups;
+    rep->max_rel_discrepancy = 0.0;
+    rep->n_flagged = rep->n_corrected = rep->n_unrecoverable = 0;
+    rep->fault_fired = 0;
+
+    Launch L = base_launch(in, out, batch, inverse ? 1 : 0);
+    L.abft = prot ? (values ? ABFT_TABLE : ABFT_WANG) : ABFT_OFF;
+    L.etw = etw;
+    L.values = values;
+    L.delta = delta;
+    L.abs_floor = abs_floor;
+    // ---- translate the fault into the launch's coordinates
+    if (fault && fault->where != TFFT_AT_NONE) {
+        const int width = p->prec == TFFT_FP32 ? 32 : 64;
+        bool fires = fault->signal >= 0 && fault->signal < batch && fault->element >= 0 && fault->element < n;
+        if (fault->where == TFFT_AT_STAGE && (fault->stage < 0 || fault->stage >= p->nstages)) fires = false;
+        if (fires) {
+            if (fault->bit < 0 || fault->bit >= width) return fail(TFFT_EINVAL, "bit out of range for the precision");
+            if (fault->component != 0 && fault->component != 1) return fail(TFFT_EINVAL, "component must be re/im");
+            L.f_signal = fault->signal;
+            L.f_comp = fault->component;
+            L.f_bit = fault->bit;
+            L.f_stage = fault->stage;
+            if (p->single) {
+                if (fault->where == TFFT_AT_INPUT) {
+                    L.f_where = AT_INPUT;
+                    L.f_elem = fault->element;
+                } else if (fault->where == TFFT_AT_OUTPUT) {
+                    L.f_where = AT_OUTPUT;
+                    L.f_elem = fault->element;
+                } else {
+                    if (fault->stage != p->nstages - 1)
+                        return fail(TFFT_EUNSUPPORTED, "intermediate-stage injection needs a multi-pass size");
+                    // last-stage hook index -> natural order
+                    const int64_t e = fault->element;
+                    int64_t f = e;
+                    if (p->nstages == 2) {
+                        const int64_t d0 = p->dims[0], d1 = p->dims[1];
+                        f = (e / d1) + d0 * (e % d1);
+                    } else if (p->nstages == 3) {
+                        const int64_t d0 = p->dims[0], d1 = p->dims[1], d2 = p->dims[2];
+                        const int64_t k0 = e / (d1 * d2), k1 = (e / d2) % d1, k2 = e % d2;
+                        f = k0 + d0 * k1 + d0 * d1 * k2;
+                    }
+                    L.f_where = AT_PRESCALE;
+                    L.f_elem = f;
+                }
+            } else {
+                L.f_where = fault->where == TFFT_AT_INPUT ? 1 : (fault->where == TFFT_AT_STAGE ? 2 : 3);
+                L.f_elem = fault->element;
+            }
+            rep->fault_fired = 1;
+        }
+    }
+    if (prot) {
+        rc = ensure_flags(p, batch);
+        if (rc) return rc;
+        CU(cudaMemsetAsync(p->d_cnt, 0, sizeof(Counters), st));
+    }
+    rc = launch_transform(p, L, st);
+    if (rc) return rc;
+    if (!prot) return TFFT_OK;
+    // the (tiny) detection summary rides back behind the transform
+    CU(cudaMemcpyAsync(p->h_cnt, p->d_cnt, sizeof(Counters), cudaMemcpyDeviceToHost, st));
+    if (!p->ev_done) CU(cudaEventCreateWithFlags(&p->ev_done, cudaEventDisableTiming));
+    CU(cudaEventRecord(p->ev_done, st));
+    return TFFT_OK;
+}
+
+int tfft_protect_finish(tfft_plan* p, const void* in, void* out, int64_t batch, int scheme, double delta,
+                        double abs_floor, const void* etw, const void* values, int inverse, tfft_report* rep,
+                        void* stream) {
+    int rc = check_plan(p);
+    if (rc) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (!rep) return fail(TFFT_EINVAL, "null report");
+    if (scheme == TFFT_SCHEME_NONE) return TFFT_OK;
+    if (!p->ev_done) return fail(TFFT_EINVAL, "tfft_protect_finish without tfft_protect_launch");
+    const int64_t n = p->n;
+    CU(cudaEventSynchronize(p->ev_done));
+    const int64_t nflag = std::min<int64_t>(p->h_cnt->flag_count, batch);
+    if (p->prec == TFFT_FP32) {
+        unsigned int k = (unsigned int)(p->h_cnt->max_key & 0xffffffffull);
+        float f;
+        memcpy(&f, &k, 4);
+        rep->max_rel_discrepancy = f;
+    } else {
+        double d;
+        memcpy(&d, &p->h_cnt->max_key, 8);
+        rep->max_rel_discrepancy = d;
+    }
+    std::vector<std::pair<long long, double>> flags;
+    if (nflag > 0) {
+        std::vector<long long> sig(nflag);
+        CU(cudaMemcpyAsync(sig.data(), p->d_flag_sig, nflag * sizeof(long long), cudaMemcpyDeviceToHost, st));
+        std::vector<double> rel(nflag);
+        if (p->prec == TFFT_FP32) {
+            std::vector<float> r32(nflag);
+            CU(cudaMemcpyAsync(r32.data(), p->d_flag_rel, nflag * sizeof(float), cudaMemcpyDeviceToHost, st));
+            CU(cudaStreamSynchronize(st));
+            for (int64_t i = 0; i < nflag; ++i) rel[i] = r32[i];
+        } else {
+            CU(cudaMemcpyAsync(rel.data(), p->d_flag_rel, nflag * sizeof(double), cudaMemcpyDeviceToHost, st));
+            CU(cudaStreamSynchronize(st));
+        }
+        for (int64_t i = 0; i < nflag; ++i) flags.emplace_back(sig[i], rel[i]);
+        std::sort(flags.begin(), flags.end());
+    }
+    // flagged list, in (group, signal) order like the reference's loop
+    rep->n_flagged = (int64_t)flags.size();
+    for (size_t i = 0; i < flags.size() && (int64_t)i < rep->flagged_cap; ++i) {
+        rep->flagged[i].group = flags[i].first / p->bs;
+        rep->flagged[i].signal = flags[i].first;
+        rep->flagged[i].discrepancy = flags[i].second;
+    }
+    // group decisions
+    std::vector<int64_t> bad_groups, fix_groups, fix_sig;
+    for (size_t i = 0; i < flags.size();) {
+        const int64_t g = flags[i].first / p->bs;
+        size_t j = i;
+        while (j < flags.size() && flags[j].first / p->bs == g) ++j;
+        if (j - i > 1) bad_groups.push_back(g);
+        else { fix_groups.push_back(g); fix_sig.push_back(flags[i].first); }
+        i = j;
+    }
+    std::vector<char> fixed_ok(fix_groups.size(), 0);
+    if (!fix_groups.empty()) {
+        if (scheme == TFFT_SCHEME_ONE_SIDED) {
+            // time redundancy: re-transform the flagged signal from the clean input
+            for (size_t i = 0; i < fix_groups.size(); ++i) {
+                Launch R = base_launch((const char*)in + fix_sig[i] * n * p->esize,
+                                       (char*)out + fix_sig[i] * n * p->esize, 1, inverse ? 1 : 0);
+                rc = launch_transform(p, R, st);
+                if (rc) return rc;
+                fixed_ok[i] = 1;
+            }
+            rep->recompute_count = (int64_t)fix_groups.size();
+            rep->pass_count += 2 * (int64_t)p->nstages * rep->recompute_count;
+        } else {
+            // two-sided: y_f = W s0 - sum_{b != f} y_b, verified before commit
+            const int64_t chunk_max = std::max<int64_t>(1, std::min<int64_t>(256, (int64_t(1) << 28) / (n * (int64_t)p->esize)));
+            for (size_t c0 = 0; c0 < fix_groups.size(); c0 += chunk_max) {
+                const int64_t K = std::min<int64_t>(chunk_max, fix_groups.size() - c0);
+                rc = ensure_scratch(p, (size_t)3 * K * n * p->esize);
+                if (rc) return rc;
+                char* s0 = (char*)p->d_scratch;
+                char* ws0 = s0 + (size_t)K * n * p->esize;
+                char* fx = ws0 + (size_t)K * n * p->esize;
+                if (K > p->jobs_cap) {
+                    cudaFree(p->d_jobs);
+                    p->d_jobs = nullptr;
+                    CU(cudaMalloc(&p->d_jobs, K * sizeof(FixJob)));
+                    p->jobs_cap = K;
+                }
+                std::vector<FixJob> jobs(K);
+                const int grid = (int)std::min<long long>((n + 255) / 256, 4LL * p->num_sms);
+                for (int64_t k = 0; k < K; ++k) {
+                    const int64_t g = fix_groups[c0 + k];
+                    jobs[k].first = g * p->bs;
+                    jobs[k].flagged = fix_sig[c0 + k];
+                    jobs[k].ok = 0;
+                    const char* xg = (const char*)in + (size_t)g * p->bs * n * p->esize;
+                    if (p->prec == TFFT_FP32)
+                        group_sums_kernel<float><<<grid, 256, 0, st>>>((const float2*)xg, p->bs, n,
+                                                                       (float2*)(s0 + k * n * p->esize), nullptr);
+                    else
+                        group_sums_kernel<double><<<grid, 256, 0, st>>>((const double2*)xg, p->bs, n,
+                                                                        (double2*)(s0 + k * n * p->esize), nullptr);
+                }
+                CU(cudaGetLastError());
+                Launch W = base_launch(s0, ws0, K, inverse ? 1 : 0);
+                rc = launch_transform(p, W, st);
+                if (rc) return rc;
+                CU(cudaMemcpyAsync(p->d_jobs, jobs.data(), K * sizeof(FixJob), cudaMemcpyHostToDevice, st));
+                if (p->prec == TFFT_FP32)
+                    fix_groups_kernel<float><<<(unsigned)K, AUX_THREADS, 0, st>>>(
+                        (const float2*)in, (float2*)out, n, p->bs, (const float2*)ws0, (float2*)fx,
+                        (const float2*)etw, (const float2*)values, (float)delta, (float)abs_floor, 1e-6f, p->d_jobs);
+                else
+                    fix_groups_kernel<double><<<(unsigned)K, AUX_THREADS, 0, st>>>(
+                        (const double2*)in, (double2*)out, n, p->bs, (const double2*)ws0, (double2*)fx,
+                        (const double2*)etw, (const double2*)values, delta, abs_floor, 1e-12, p->d_jobs);
+                CU(cudaGetLastError());
+                CU(cudaMemcpyAsync(jobs.data(), p->d_jobs, K * sizeof(FixJob), cudaMemcpyDeviceToHost, st));
+                CU(cudaStreamSynchronize(st));
+                for (int64_t k = 0; k < K; ++k) fixed_ok[c0 + k] = (char)jobs[k].ok;
+            }
+        }
+    }
+    // corrected / unrecoverable lists in group order
+    std::vector<int64_t> unrec = bad_groups;
+    int64_t nc = 0;
+    for (size_t i = 0; i < fix_groups.size(); ++i) {
+        if (fixed_ok[i]) {
+            if (nc < rep->corrected_cap) {
+                rep->corrected_group[nc] = fix_groups[i];
+                rep->corrected_signal[nc] = fix_sig[i];
+            }
+            ++nc;
+        } else {
+            unrec.push_back(fix_groups[i]);
+        }
+    }
+    std::sort(unrec.begin(), unrec.end());
+    rep->n_corrected = nc;
+    rep->n_unrecoverable = (int64_t)unrec.size();
+    for (size_t i = 0; i < unrec.size() && (int64_t)i < rep->unrecoverable_cap; ++i) rep->unrecoverable[i] = unrec[i];
+    return TFFT_OK;
+}
+
+namespace {
+struct TileCache {
+    std::mutex mu;
+    std::map<std::pair<int64_t, int>, tfft_plan*> plans;
+    void* d_buf = nullptr;
+    size_t d_bytes = 0;
+};
+TileCache g_tile;
+}  // namespace
+
+int tfft_tile_fft(const void* in, void* out, int64_t t, int64_t l, int dtype_bytes, int inverse, int host,
+                  void* stream) {
+    if (dtype_bytes != 8 && dtype_bytes != 16) return fail(TFFT_EINVAL, "unsupported dtype");
+    if (t < 0 || l < 1 || !is_pow2(l)) return fail(TFFT_EINVAL, "tiles must be (T, L) with L a power of two");
+    if (t == 0) return TFFT_OK;
+    if (!in || !out) return fail(TFFT_EINVAL, "null buffer");
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t bytes = (size_t)t * l * dtype_bytes;
+    if (l == 1) {
+        CU(cudaMemcpyAsync(out, in, bytes, host ? cudaMemcpyHostToHost : cudaMemcpyDeviceToDevice, st));
+        if (host) CU(cudaStreamSynchronize(st));
+        return TFFT_OK;
+    }
+    std::lock_guard<std::mutex> lk(g_tile.mu);
+    const int prec = dtype_bytes == 8 ? TFFT_FP32 : TFFT_FP64;
+    auto key = std::make_pair(l, prec);
+    tfft_plan* p;
+    auto it = g_tile.plans.find(key);
+    if (it == g_tile.plans.end()) {
+        const int e = ilog2(l);
+        const int cnt = l <= (1 << 13) ? 1 : (l <= (1 << 22) ? 2 : 3);
+        int64_t dims[3];
+        const int base = e / cnt, rem = e % cnt;
+        for (int i = 0; i < cnt; ++i) dims[i] = int64_t(1) << (base + (i >= cnt - rem ? 1 : 0));
+        int device = 0;
+        CU(cudaGetDevice(&device));
+        int rc = tfft_plan_create(&p, l, prec, cnt, dims, 1, device);
+        if (rc) return rc;
+        g_tile.plans[key] = p;
+    } else {
+        p = it->second;
+    }
+    const void* din = in;
+    void* dout = out;
+    if (host) {
+        if (2 * bytes > g_tile.d_bytes) {
+            cudaFree(g_tile.d_buf);
+            g_tile.d_buf = nullptr;
+            g_tile.d_bytes = 0;
+            CU(cudaMalloc(&g_tile.d_buf, 2 * bytes));
+            g_tile.d_bytes = 2 * bytes;
+        }
+        CU(cudaMemcpyAsync(g_tile.d_buf, in, bytes, cudaMemcpyHostToDevice, st));
+        din = g_tile.d_buf;
+        dout = (char*)g_tile.d_buf + bytes;
+    }
+    Launch L = base_launch(din, dout, t, inverse ? 1 : 0);
+    L.scale_inv = 0;  // tile_fft leaves scaling to the caller (_stockham.pyx:46-65)
+    int rc = launch_transform(p, L, st);
+    if (rc) return rc;
+    if (host) {
+        CU(cudaMemcpyAsync(out, dout, bytes, cudaMemcpyDeviceToHost, st));
+        CU(cudaStreamSynchronize(st));
+    }
+    return TFFT_OK;
+}
+
+}  // extern "C"

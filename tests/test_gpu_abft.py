@@ -1,0 +1,239 @@
+"""GPU ABFT parity: detection / correction decisions under identical injected
+faults must equal the reference's (bit-exact decisions), outputs within the
+stated tolerance, and the reference's fusion / pass-count contracts hold."""
+
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import ROOT, random_batch, rel_l2
+from golden.make_golden import protected_input
+
+pytestmark = pytest.mark.gpu
+
+from paper_2405_02520_b200.abft import (DetectionConfig, Scheme, UnrecoverableError,  # noqa: E402
+                                        correct_group, detect, encode_group, finalize_group,
+                                        make_encoding, run_protected)
+from paper_2405_02520_b200.fault_lab import BitFlipInjector, FaultSpec  # noqa: E402
+from paper_2405_02520_b200.fft_core import (build_twiddles, fft_execute, fit_group_size,  # noqa: E402
+                                            make_plan)
+
+GOLD = os.path.join(ROOT, "tests", "golden")
+TOL = {"fp32": 1e-5, "fp64": 1e-12}
+
+
+def decisions(rep):
+    d = rep if isinstance(rep, dict) else json.loads(rep.to_json())
+    return ([(f["group"], f["signal"]) for f in d["flagged"]],
+            [(c["group"], c["signal"]) for c in d["corrected"]],
+            list(d["unrecoverable"]), d["recompute_count"], d["pass_count"])
+
+
+def test_golden_protected_cases():
+    from oracle import port as P
+    cases = json.load(open(os.path.join(GOLD, "protected.json")))
+    arrays = np.load(os.path.join(GOLD, "protected.npz"))
+    for c in cases:
+        x = protected_input(c["id"], c["n"], c["batch"], c["precision"])
+        plan = fit_group_size(make_plan(c["n"], c["precision"], batch=c["batch"]), c["batch"])
+        inj = None
+        if c["fault"] is not None:
+            s, el, comp, bit, stage = c["fault"]
+            inj = BitFlipInjector(FaultSpec(0, s, el, comp, bit, stage))
+        cfg = DetectionConfig(delta=1e-4 if c["precision"] == "fp32" else 1e-9)
+        out, rep, cnt = run_protected(plan, build_twiddles(plan), torch.from_numpy(x).cuda(),
+                                      c["scheme"], cfg, injector=inj, inverse=c["inverse"])
+        assert decisions(rep) == decisions(c["report"]), c["id"]
+        assert cnt.total == c["pass_total"]
+        assert (inj.fired if inj else False) == c["fired"]
+        for mine, theirs in zip(rep.flagged, c["report"]["flagged"]):
+            if math.isinf(theirs["discrepancy"]):
+                assert math.isinf(mine["discrepancy"])
+            else:
+                assert mine["discrepancy"] == pytest.approx(theirs["discrepancy"], rel=1e-3)
+        key = f"c{c['id']}_y"
+        if key in arrays:
+            ref = arrays[key]
+        else:  # oracle (pinned bit-exact to the reference by test_oracle.py)
+            op = P.shrink_bs(P.plan_for(c["n"], c["precision"], batch=c["batch"]), c["batch"])
+            oinj = P.OneShot(*c["fault"]) if c["fault"] else None
+            ref, _, _ = P.protected(op, P.twiddles_for(op), x, c["scheme"],
+                                    delta=cfg.delta, injector=oinj, inverse=c["inverse"])
+        tol = TOL[c["precision"]] * math.log2(c["n"]) * (10 if c["report"]["corrected"] else 1)
+        assert rel_l2(out, ref) <= tol, (c["id"], rel_l2(out, ref))
+
+
+@pytest.mark.parametrize("n,prec", [(16, "fp32"), (256, "fp32"), (1024, "fp32"), (8192, "fp64"),
+                                    (2**14, "fp64"), (2**17, "fp32"), (2**23, "fp32")])
+def test_fusion_bitwise_and_pass_count(n, prec):
+    b = 16 if n <= 2**17 else 2
+    x = random_batch(np.random.default_rng(5), (b, n), np.complex64 if prec == "fp32"
+                     else np.complex128)
+    plan = make_plan(n, prec, batch=b)
+    plan = fit_group_size(plan, b)
+    tw = build_twiddles(plan)
+    xd = torch.from_numpy(x).cuda()
+    cfg = DetectionConfig(delta=1e-4 if prec == "fp32" else 1e-9)
+    clean, _, c0 = run_protected(plan, tw, xd, Scheme.NONE, cfg)
+    prot, rep, c2 = run_protected(plan, tw, xd, Scheme.TWO_SIDED_GROUP, cfg)
+    assert torch.equal(clean, prot)
+    assert c0.total == c2.total == 2 * len(plan.stages) * (b // plan.bs)
+    assert rep.flagged == [] and rep.recompute_count == 0
+    assert 0 < rep.max_rel_discrepancy < cfg.delta
+    assert torch.equal(clean, fft_execute(plan, tw, xd))
+
+
+def test_exponent_bit_flips_all_detected_and_corrected():
+    """Reference acceptance 04 (tests/test_acceptance.py:104-141), with every
+    decision also compared against the oracle."""
+    from oracle import port as P
+    plan = make_plan(256, "fp32", batch=8)
+    tw = build_twiddles(plan)
+    op = P.plan_for(256, "fp32", batch=8)
+    otw = P.twiddles_for(op)
+    cfg = DetectionConfig(delta=1e-4)
+    detected = corrected = rec_two = rec_one = 0
+    total = 200
+    for i in range(total):
+        rng = np.random.default_rng([77, i])
+        x = random_batch(rng, (8, 256), np.complex64)
+        spec = FaultSpec(i, int(rng.integers(8)), int(rng.integers(256)),
+                         "re" if rng.integers(2) == 0 else "im", int(rng.integers(25, 31)))
+        xd = torch.from_numpy(x).cuda()
+        clean, _, _ = run_protected(plan, tw, xd, Scheme.NONE, cfg)
+        out, rep, _ = run_protected(plan, tw, xd, Scheme.TWO_SIDED_GROUP, cfg,
+                                    injector=BitFlipInjector(spec))
+        _, orep, _ = P.protected(op, otw, x, "two_sided_group", delta=1e-4,
+                                 injector=P.OneShot(spec.signal_idx, spec.element_idx,
+                                                    spec.component, spec.bit))
+        assert decisions(rep) == decisions(orep)
+        rec_two += rep.recompute_count
+        if rep.flagged:
+            detected += 1
+            if rel_l2(out, clean) <= 1e-4:
+                corrected += 1
+        _, rep1, _ = run_protected(plan, tw, xd, Scheme.ONE_SIDED, cfg,
+                                   injector=BitFlipInjector(spec))
+        rec_one += rep1.recompute_count
+    assert detected == total and corrected == detected
+    assert rec_two == 0 and rec_one == detected
+
+
+@pytest.mark.parametrize("n,prec,stage", [(2**14, "fp64", "stage:0"), (2**14, "fp32", "stage:1"),
+                                          (2**23, "fp64", "stage:1"), (2**20, "fp64", "input"),
+                                          (2**25, "fp32", "output"), (2**23, "fp32", "stage:2")])
+def test_multipass_injection_corrected(n, prec, stage):
+    b = 2
+    x = random_batch(np.random.default_rng(n), (b, n), np.complex64 if prec == "fp32"
+                     else np.complex128)
+    plan = fit_group_size(make_plan(n, prec, batch=b), b)
+    tw = build_twiddles(plan)
+    xd = torch.from_numpy(x).cuda()
+    cfg = DetectionConfig(delta=1e-4 if prec == "fp32" else 1e-9)
+    clean, _, _ = run_protected(plan, tw, xd, Scheme.NONE, cfg)
+    bit = 30 if prec == "fp32" else 62
+    inj = BitFlipInjector(FaultSpec(0, 1, n // 3 + 7, "re", bit, stage))
+    out, rep, _ = run_protected(plan, tw, xd, Scheme.TWO_SIDED_GROUP, cfg, injector=inj)
+    assert inj.fired
+    assert [c["signal"] for c in rep.corrected] == [1], rep.to_json()
+    assert rel_l2(out, clean) <= TOL[prec] * math.log2(n) * 10
+
+
+def test_double_fault_unrecoverable_generic_callable():
+    plan = fit_group_size(make_plan(256, "fp64", batch=8), 8)
+    x = random_batch(np.random.default_rng(1), (8, 256))
+
+    def double_fault(where, group_start, buf):
+        if where == "output":
+            buf[0, 0] += 100.0
+            buf[3, 9] += 100.0
+
+    out, rep, _ = run_protected(plan, build_twiddles(plan), torch.from_numpy(x).cuda(),
+                                Scheme.TWO_SIDED_GROUP, DetectionConfig(delta=1e-9),
+                                injector=double_fault)
+    assert rep.unrecoverable == [0] and rep.corrected == []
+
+
+def test_generic_callable_matches_fused_path():
+    plan = fit_group_size(make_plan(2**14, "fp64", batch=4), 4)
+    tw = build_twiddles(plan)
+    x = torch.from_numpy(random_batch(np.random.default_rng(2), (4, 2**14))).cuda()
+    cfg = DetectionConfig(delta=1e-9)
+    spec = FaultSpec(0, 2, 999, "re", 62, "stage:0")
+    a, ra, ca = run_protected(plan, tw, x, Scheme.TWO_SIDED_GROUP, cfg,
+                              injector=BitFlipInjector(spec))
+    inj = BitFlipInjector(spec)
+    b, rb, cb = run_protected(plan, tw, x, Scheme.TWO_SIDED_GROUP, cfg,
+                              injector=lambda w, s, buf: inj(w, s, buf))
+    assert decisions(ra) == decisions(rb) and ca.total == cb.total
+    assert rel_l2(a, b) <= 1e-13
+
+
+def test_pipeline_api_zero_batch_and_inf():
+    plan = make_plan(8, "fp64")
+    tw = build_twiddles(plan)
+    enc = make_encoding("ones", 8)
+    xg = torch.zeros(4, 8, dtype=torch.complex128, device="cuda")
+    state = encode_group(xg, enc)
+    yg = fft_execute(plan, tw, xg)
+    yg[1, 2] += 1.0
+    finalize_group(state, yg)
+    fixed = correct_group(state, yg, 1, plan, tw, enc, DetectionConfig(delta=1e-4, abs_floor=1e-12))
+    assert torch.equal(fixed, torch.zeros_like(fixed))
+    rng = np.random.default_rng(0)
+    x = torch.from_numpy(random_batch(rng, (4, 8))).cuda()
+    st = encode_group(x, enc)
+    y = fft_execute(plan, tw, x)
+    y[1, 0] = float("inf")
+    rep = detect(st, y, enc, DetectionConfig(delta=1e30))
+    assert [f.signal_idx for f in rep.flagged] == [1]
+
+
+def test_pipeline_api_unit_fault_and_corrupted_checksum():
+    plan = make_plan(8, "fp64")
+    tw = build_twiddles(plan)
+    enc = make_encoding("ones", 8)
+    x = torch.from_numpy(random_batch(np.random.default_rng(3), (4, 8))).cuda()
+    clean = fft_execute(plan, tw, x)
+    st = encode_group(x, enc)
+    y = clean.clone()
+    y[0, 0] += 1.0
+    rep = detect(st, y, enc, DetectionConfig(delta=1e-4))
+    assert [f.signal_idx for f in rep.flagged] == [0]
+    assert abs(abs(rep.flagged[0].epsilon_estimate) - 1.0) < 1e-9
+    y2 = clean.clone()
+    y2[2, 5] += 1.0
+    fixed = correct_group(st, y2, 2, plan, tw, enc, DetectionConfig(delta=1e-4))
+    assert rel_l2(fixed, clean) <= 1e-10
+    y3 = clean.clone()
+    y3[0] += 1.0
+    y3[3, 1] += 5.0
+    with pytest.raises(UnrecoverableError):
+        correct_group(st, y3, 3, plan, tw, enc, DetectionConfig(delta=1e-4))
+
+
+def test_encodings_match_reference_golden():
+    g = np.load(os.path.join(GOLD, "encodings.npz"))
+    for kind in ("wang", "ones", "jou", "linear"):
+        for n in (2, 4, 16, 1024):
+            enc = make_encoding(kind, n)
+            ref = g[f"{kind}_{n}_etw"]
+            scale = max(np.abs(ref).max(), 1.0)
+            assert np.abs(enc.etw - ref).max() <= 1e-12 * scale
+            assert np.abs(enc.etw_inv - g[f"{kind}_{n}_etw_inv"]).max() <= 1e-12 * scale
+
+
+def test_zero_signals_flag_without_floor():
+    """rel = 0/0 -> NaN -> inf flags (reference pipeline.py:116-121)."""
+    plan = fit_group_size(make_plan(64, "fp32", batch=4), 4)
+    x = torch.zeros(4, 64, dtype=torch.complex64, device="cuda")
+    _, rep, _ = run_protected(plan, build_twiddles(plan), x, Scheme.TWO_SIDED_GROUP)
+    assert [f["signal"] for f in rep.flagged] == [0, 1, 2, 3]
+    assert rep.unrecoverable == [0]
+    _, rep2, _ = run_protected(plan, build_twiddles(plan), x, Scheme.TWO_SIDED_GROUP,
+                               DetectionConfig(delta=1e-4, abs_floor=1e-12))
+    assert rep2.flagged == []

@@ -1,0 +1,173 @@
+"""GPU transform parity: the CUDA path (through the C ABI) against the
+reference's golden outputs, the oracle, and size-independent properties at
+full sizes. Tolerances follow the north star: rel-L2 <= 1e-5 (fp32) /
+1e-12 (fp64) scaled by log2 N; tighter accuracy bounds are asserted too."""
+
+import math
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import ROOT, random_batch, rel_l2
+from golden.make_golden import fft_input
+
+pytestmark = pytest.mark.gpu
+
+import paper_2405_02520_b200 as T  # noqa: E402
+from paper_2405_02520_b200.fft_core import build_twiddles, fft_execute, make_plan  # noqa: E402
+
+GOLD = os.path.join(ROOT, "tests", "golden")
+TOL = {"fp32": 1e-5, "fp64": 1e-12}
+# accuracy we actually hold ourselves to (the reference itself is ~1e-8 / ~1e-16 * log2 N)
+ACC = {"fp32": 2e-7, "fp64": 1e-15}
+DT = {"fp32": np.complex64, "fp64": np.complex128}
+
+
+def run(n, prec, x, inverse=False):
+    plan = make_plan(n, prec)
+    return fft_execute(plan, build_twiddles(plan), x, inverse=inverse)
+
+
+@pytest.fixture(scope="module")
+def gold():
+    return np.load(os.path.join(GOLD, "fft.npz"))
+
+
+@pytest.mark.parametrize("prec", ["fp32", "fp64"])
+def test_matches_reference_golden(gold, prec):
+    for e in range(1, 16 if prec == "fp64" else 15):
+        x = fft_input(prec, e)
+        y = run(2**e, prec, torch.from_numpy(x).cuda())
+        ref = gold[f"{prec}_{e}_y"]
+        err = rel_l2(y, ref)
+        assert err <= TOL[prec] * e, (prec, e, err)
+        exact = np.fft.fft(x.astype(np.complex128), axis=-1)
+        assert rel_l2(y, exact) <= ACC[prec] * max(e, 1), (prec, e, rel_l2(y, exact))
+        if e <= 12:
+            yi = run(2**e, prec, torch.from_numpy(x).cuda(), inverse=True)
+            assert rel_l2(yi, gold[f"{prec}_{e}_yi"]) <= TOL[prec] * e
+
+
+@pytest.mark.parametrize("prec", ["fp32", "fp64"])
+@pytest.mark.parametrize("e", [16, 17, 18, 20, 21, 22, 23, 24, 25])
+def test_large_sizes_against_fp64_oracle(prec, e):
+    n = 2**e
+    b = 2 if e <= 22 else 1
+    rng = np.random.default_rng(e)
+    x = random_batch(rng, (b, n), DT[prec])
+    y = run(n, prec, torch.from_numpy(x).cuda())
+    exact = np.fft.fft(x.astype(np.complex128), axis=-1)
+    err = rel_l2(y, exact)
+    assert err <= ACC[prec] * e, (prec, e, err)
+    back = run(n, prec, y, inverse=True)
+    assert rel_l2(back, x) <= 2 * ACC[prec] * e
+
+
+def test_kats_on_gpu():
+    x = torch.zeros(4, dtype=torch.complex128, device="cuda")
+    x[0] = 1
+    np.testing.assert_allclose(run(4, "fp64", x).cpu().numpy(), np.ones(4), atol=1e-12)
+    np.testing.assert_allclose(run(4, "fp64", torch.ones(4, dtype=torch.complex128, device="cuda"))
+                               .cpu().numpy(), [4, 0, 0, 0], atol=1e-12)
+    y = run(2, "fp64", torch.tensor([3 + 1j, 1 - 2j], dtype=torch.complex128, device="cuda"))
+    np.testing.assert_allclose(y.cpu().numpy(), [4 - 1j, 2 + 3j], atol=1e-12)
+    for n in (2, 8, 1024, 2**14, 2**20):
+        d = torch.zeros(n, dtype=torch.complex128, device="cuda")
+        d[0] = 1
+        np.testing.assert_allclose(run(n, "fp64", d).cpu().numpy(), np.ones(n), atol=1e-9)
+
+
+@pytest.mark.parametrize("n,b", [(8, 1000), (64, 7), (1024, 33), (8192, 3), (2**14, 3)])
+def test_ragged_batches_and_host_roundtrip(n, b):
+    rng = np.random.default_rng(n + b)
+    x = random_batch(rng, (b, n), np.complex64)
+    keep = x.copy()
+    y = run(n, "fp32", x)                      # numpy in -> numpy out
+    assert isinstance(y, np.ndarray) and y.dtype == np.complex64
+    np.testing.assert_array_equal(x, keep)     # input never written
+    assert rel_l2(y, np.fft.fft(x.astype(np.complex128))) <= ACC["fp32"] * math.log2(n)
+
+
+def test_device_input_not_mutated():
+    for n in (256, 2**16):
+        x = torch.randn(4, n, dtype=torch.complex128, device="cuda")
+        keep = x.clone()
+        run(n, "fp64", x)
+        assert torch.equal(x, keep)
+
+
+@pytest.mark.parametrize("n", [64, 4096, 2**15, 2**23])
+def test_linearity_and_parseval(n):
+    g = torch.Generator(device="cuda").manual_seed(n)
+    x = torch.randn(2, n, dtype=torch.complex128, device="cuda", generator=g)
+    z = torch.randn(2, n, dtype=torch.complex128, device="cuda", generator=g)
+    a, b = 0.75 - 0.5j, -2.0 + 0.25j
+    lhs = run(n, "fp64", a * x + b * z)
+    rhs = a * run(n, "fp64", x) + b * run(n, "fp64", z)
+    assert rel_l2(lhs, rhs) <= 1e-14 * math.log2(n)
+    y = run(n, "fp64", x)
+    e_x = float((x.abs() ** 2).sum())
+    e_y = float((y.abs() ** 2).sum()) / n
+    assert abs(e_x - e_y) <= 1e-12 * e_x
+
+
+def test_explicit_three_stage_plan_and_max_tile():
+    from paper_2405_02520_b200.fft_core import FftPlan, Stage
+    plan = FftPlan(4096, (Stage(16, 16), Stage(16, 16), Stage(16, 16)), 4, "fp64", "direct")
+    x = random_batch(np.random.default_rng(1), (1, 4096))
+    y = fft_execute(plan, build_twiddles(plan), x)
+    assert rel_l2(y, np.fft.fft(x)) <= 1e-14
+
+
+def test_on_stage_hook_views_match_reference_layout():
+    from oracle import port as P
+    for n, prec in ((2**14, "fp64"), (2**17, "fp32"), (2**23, "fp64"), (1024, "fp32")):
+        b = 2 if n < 2**20 else 1
+        x = random_batch(np.random.default_rng(n), (b, n), DT[prec])
+        views_gpu, views_ref = {}, {}
+        plan = make_plan(n, prec)
+        y = fft_execute(plan, build_twiddles(plan), torch.from_numpy(x).cuda(),
+                        on_stage=lambda k, v: views_gpu.__setitem__(k, v.cpu().numpy().copy()))
+        oplan = P.plan_for(n, prec)
+        if n <= 2**22:
+            P.execute(oplan, P.twiddles_for(oplan), x,
+                      hook=lambda k, v: views_ref.__setitem__(k, v.copy()))
+        else:
+            P.execute(oplan, P.twiddles_for(oplan), x, cap=2**25,
+                      hook=lambda k, v: views_ref.__setitem__(k, v.copy()))
+        assert sorted(views_gpu) == sorted(views_ref) == list(range(len(plan.stages)))
+        for k in views_ref:
+            assert rel_l2(views_gpu[k], views_ref[k]) <= TOL[prec] * math.log2(n), (n, k)
+        fused = fft_execute(plan, build_twiddles(plan), torch.from_numpy(x).cuda())
+        assert torch.equal(y, fused)  # staged execution is the same arithmetic
+
+
+def test_tile_fft_plugin_contract():
+    from paper_2405_02520_b200.kernels import get_backend
+    be = get_backend("cuda")
+    rng = np.random.default_rng(3)
+    for length in (2, 4, 8, 64, 512, 4096):
+        for dt in (np.complex64, np.complex128):
+            tiles = random_batch(rng, (4, length), dt)
+            keep = tiles.copy()
+            base = np.exp(-2j * np.pi * np.arange(length // 2) / length).astype(dt)
+            out = be.tile_fft(tiles, base)
+            np.testing.assert_array_equal(tiles, keep)
+            tol = 1e-5 if dt == np.complex64 else 1e-12
+            assert rel_l2(out, np.fft.fft(tiles.astype(np.complex128))) <= tol
+            inv = be.tile_fft(tiles, base, inverse=True)  # unscaled
+            assert rel_l2(inv, np.fft.ifft(tiles.astype(np.complex128)) * length) <= tol
+    with pytest.raises(TypeError):
+        be.tile_fft(np.zeros((2, 4), np.float32), None)
+    one = random_batch(rng, (3, 1), np.complex64)
+    np.testing.assert_array_equal(be.tile_fft(one, np.zeros(0, np.complex64)), one)
+
+
+def test_rejects_bad_input():
+    plan = make_plan(16, "fp64")
+    with pytest.raises(ValueError):
+        fft_execute(plan, build_twiddles(plan), np.zeros(8, np.complex128))
+    with pytest.raises(ValueError):
+        fft_execute(plan, build_twiddles(plan), np.zeros((2, 16)), backend="opencl")
