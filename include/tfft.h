@@ -162,6 +162,13 @@ int tfft_execute_stage(tfft_plan *plan, int k, const void *in, void *out, int64_
 /* buf[i] *= s for count complex elements (the inverse 1/n, execute.py:77-78). */
 int tfft_scale(void *buf, int64_t count, int dtype_bytes, double s, void *stream);
 
+/* Tuning hooks of the plan generator (paper_2405_02520_b200/codegen.py):
+ * number of compiled launch variants of the single-kernel size 2^logn, and a
+ * process-wide override of which one launches (variant < 0 restores the
+ * tuned default). Used by tools/tune.py; not needed by callers. */
+int tfft_tune_variants(int precision, int logn);
+int tfft_tune_select(int precision, int logn, int variant);
+
 const char *tfft_last_error(void);
 int tfft_version(void);
 

@@ -19,23 +19,64 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 
-# (E, radices, threads) per log2 N for the single-kernel path (N <= 2^13).
-SINGLE_TABLE = {
+# Single-kernel path (N <= 2^13): candidate launch configurations per
+# (precision, log2 N) as (E, radices, threads, min CTAs/SM, staged I/O).
+# Candidate 0 is the default; tools/tune.py times all of them on the B200
+# and SINGLE_CHOICE records the winner (index into the candidate list).
+def _cands(*rows):
+    return [dict(e=r[0], radices=tuple(r[1]), threads=r[2], minb=r[3], stage=r[4]) for r in rows]
+
+
+SINGLE_CANDIDATES = {
     "fp32": {
-        1: (2, (2,), 256), 2: (4, (4,), 256), 3: (8, (8,), 256), 4: (16, (16,), 256),
-        5: (8, (8, 4), 256), 6: (8, (8, 8), 256), 7: (16, (16, 8), 256),
-        8: (16, (16, 16), 256), 9: (32, (32, 16), 256), 10: (32, (32, 32), 256),
-        11: (16, (16, 16, 8), 256), 12: (16, (16, 16, 16), 256),
-        13: (32, (32, 16, 16), 256),
+        1: _cands((2, (2,), 256, 1, 1), (2, (2,), 256, 1, 0)),
+        2: _cands((4, (4,), 256, 1, 1), (4, (4,), 256, 1, 0)),
+        3: _cands((8, (8,), 256, 1, 1), (8, (8,), 256, 1, 0), (4, (4, 2), 256, 1, 1),
+                  (8, (8,), 128, 1, 1)),
+        4: _cands((16, (16,), 256, 1, 1), (16, (16,), 256, 1, 0), (8, (8, 2), 256, 1, 1),
+                  (4, (4, 4), 256, 1, 1), (16, (16,), 128, 1, 1)),
+        5: _cands((8, (8, 4), 256, 1, 1), (8, (8, 4), 256, 1, 0), (16, (16, 2), 256, 1, 1),
+                  (32, (32,), 256, 1, 1)),
+        6: _cands((8, (8, 8), 256, 1, 1), (8, (8, 8), 256, 1, 0), (16, (16, 4), 256, 1, 1),
+                  (16, (16, 4), 256, 1, 0)),
+        7: _cands((16, (16, 8), 256, 1, 0), (16, (16, 8), 256, 1, 1), (8, (8, 8, 2), 256, 1, 0),
+                  (16, (16, 8), 256, 3, 0)),
+        8: _cands((16, (16, 16), 256, 1, 0), (16, (16, 16), 256, 3, 0), (8, (8, 8, 4), 256, 1, 0),
+                  (16, (16, 16), 256, 1, 1)),
+        9: _cands((16, (16, 16, 2), 256, 2, 0), (32, (32, 16), 256, 1, 0),
+                  (8, (8, 8, 8), 256, 3, 0), (16, (16, 16, 2), 256, 3, 0)),
+        10: _cands((16, (16, 16, 4), 256, 2, 0), (32, (32, 32), 256, 1, 0),
+                   (16, (16, 16, 4), 256, 3, 0), (8, (8, 8, 8, 2), 256, 2, 0),
+                   (16, (16, 16, 4), 512, 1, 0)),
+        11: _cands((16, (16, 16, 8), 256, 2, 0), (16, (16, 16, 8), 256, 3, 0),
+                   (8, (8, 8, 8, 4), 256, 3, 0), (16, (16, 16, 8), 512, 1, 0)),
+        12: _cands((16, (16, 16, 16), 256, 2, 0), (16, (16, 16, 16), 256, 3, 0),
+                   (8, (8, 8, 8, 8), 512, 2, 0), (16, (16, 16, 16), 512, 1, 0)),
+        13: _cands((16, (16, 16, 16, 2), 512, 2, 0), (32, (32, 16, 16), 256, 1, 0),
+                   (16, (16, 16, 16, 2), 512, 1, 0), (8, (8, 8, 8, 8, 2), 1024, 1, 0)),
     },
     "fp64": {
-        1: (2, (2,), 256), 2: (4, (4,), 256), 3: (8, (8,), 256), 4: (16, (16,), 256),
-        5: (8, (8, 4), 256), 6: (8, (8, 8), 256), 7: (16, (16, 8), 256),
-        8: (16, (16, 16), 256), 9: (8, (8, 8, 8), 256), 10: (16, (16, 16, 4), 256),
-        11: (16, (16, 16, 8), 256), 12: (16, (16, 16, 16), 256),
-        13: (16, (16, 16, 16, 2), 512),
+        1: _cands((2, (2,), 256, 1, 1), (2, (2,), 256, 1, 0)),
+        2: _cands((4, (4,), 256, 1, 1), (4, (4,), 256, 1, 0)),
+        3: _cands((8, (8,), 256, 1, 1), (8, (8,), 256, 1, 0), (4, (4, 2), 256, 1, 1)),
+        4: _cands((16, (16,), 256, 1, 1), (8, (8, 2), 256, 1, 1), (4, (4, 4), 256, 1, 1)),
+        5: _cands((8, (8, 4), 256, 1, 1), (8, (8, 4), 256, 1, 0), (16, (16, 2), 256, 1, 1)),
+        6: _cands((8, (8, 8), 256, 1, 1), (8, (8, 8), 256, 1, 0), (16, (16, 4), 256, 1, 0)),
+        7: _cands((16, (16, 8), 256, 1, 0), (8, (8, 8, 2), 256, 1, 0), (16, (16, 8), 256, 1, 1)),
+        8: _cands((16, (16, 16), 256, 1, 0), (8, (8, 8, 4), 256, 1, 0), (16, (16, 16), 256, 2, 0)),
+        9: _cands((8, (8, 8, 8), 256, 1, 0), (16, (16, 16, 2), 256, 1, 0),
+                  (8, (8, 8, 8), 256, 3, 0)),
+        10: _cands((16, (16, 16, 4), 256, 1, 0), (8, (8, 8, 8, 2), 256, 1, 0),
+                   (16, (16, 16, 4), 256, 2, 0)),
+        11: _cands((16, (16, 16, 8), 256, 1, 0), (16, (16, 16, 8), 256, 2, 0),
+                   (8, (8, 8, 8, 4), 256, 2, 0)),
+        12: _cands((16, (16, 16, 16), 256, 1, 0), (16, (16, 16, 16), 512, 1, 0),
+                   (8, (8, 8, 8, 8), 512, 1, 0)),
+        13: _cands((16, (16, 16, 16, 2), 512, 1, 0), (8, (8, 8, 8, 8, 2), 1024, 1, 0)),
     },
 }
+# tuned winners (index into SINGLE_CANDIDATES[prec][logn]); missing -> 0
+SINGLE_CHOICE = {"fp32": {}, "fp64": {}}
 ELEM_BYTES = {"fp32": 8, "fp64": 16}
 CTYPE = {"fp32": "float", "fp64": "double"}
 
@@ -103,24 +144,32 @@ def choose_padding(n, e, radices, prec):
     return best
 
 
-def single_configs():
+def single_configs(all_candidates=True):
+    """Every candidate (all_candidates) or only the chosen one per size."""
     out = []
-    for prec, table in SINGLE_TABLE.items():
-        for logn, (e, radices, threads) in sorted(table.items()):
-            n = 1 << logn
-            assert math.prod(radices) == n and all(e % r == 0 for r in radices)
-            tps = n // e
-            threads = max(threads, tps)
-            ps, _ = choose_padding(n, e, radices, prec)
-            s = threads // tps
-            slen = (n + (n >> ps) + 1 if ps else n) if len(radices) > 1 else 0
-            smem = s * slen * ELEM_BYTES[prec] + (threads // 32 + 1) * (ELEM_BYTES[prec] // 2)
-            out.append(dict(prec=prec, logn=logn, n=n, e=e, radices=radices,
-                            threads=threads, ps=ps, smem=smem, tps=tps))
+    for prec, table in SINGLE_CANDIDATES.items():
+        for logn, cands in sorted(table.items()):
+            chosen = SINGLE_CHOICE[prec].get(logn, 0)
+            for vi, c in enumerate(cands):
+                if not all_candidates and vi != chosen:
+                    continue
+                n = 1 << logn
+                e, radices = c["e"], c["radices"]
+                assert math.prod(radices) == n and all(e % r == 0 for r in radices), (prec, logn, c)
+                tps = n // e
+                threads = max(c["threads"], tps)
+                ps, _ = choose_padding(n, e, radices, prec)
+                s = threads // tps
+                ex = (n + (n >> ps) + 1 if ps else n) if len(radices) > 1 else 0
+                st = n + 1 if c["stage"] else 0
+                smem = s * max(ex, st) * ELEM_BYTES[prec] + (threads // 32 + 1) * (ELEM_BYTES[prec] // 2)
+                out.append(dict(prec=prec, logn=logn, n=n, e=e, radices=radices, threads=threads,
+                                ps=ps, smem=smem, tps=tps, minb=c["minb"], stage=c["stage"],
+                                variant=vi, chosen=vi == chosen))
     return out
 
 
-def _emit_single(prec, cfgs):
+def _emit_single(prec, cfgs, part, table=False):
     t = CTYPE[prec]
     lines = [
         "// GENERATED by paper_2405_02520_b200/codegen.py — do not edit.",
@@ -133,15 +182,37 @@ def _emit_single(prec, cfgs):
         rl = ", ".join(str(r) for r in c["radices"])
         fns = []
         for abft in (0, 1, 2):
+            if abft == 2 and not c["chosen"]:
+                fns.append("nullptr")  # table encodings only on the chosen config
+                continue
             fns.append(f"(const void*)&fft_single_kernel<{t}, {c['n']}, {c['e']}, {c['ps']}, "
-                       f"{abft}, {c['threads']}, RList<{rl}>>")
+                       f"{abft}, {c['threads']}, {c['minb']}, {c['stage']}, RList<{rl}>>")
         entries.append(
-            f"    {{{c['logn']}, {c['e']}, {c['threads']}, {c['smem']}, {c['tps']}, "
-            f"{{{', '.join(fns)}}}}},  // radices {rl}, pad 2^{c['ps']}")
-    lines.append(f"const SingleEntry kSingle_{prec}[] = {{")
+            f"    {{{c['logn']}, {c['variant']}, {int(c['chosen'])}, {c['e']}, {c['threads']}, "
+            f"{c['smem']}, {c['tps']}, {{{', '.join(fns)}}}}},  // radices {rl}, pad 2^{c['ps']}, "
+            f"minb {c['minb']}, stage {c['stage']}")
+    lines.append(f"extern const SingleEntry kSingle_{prec}_{part}[] = {{")
     lines += entries
     lines.append("};")
-    lines.append(f"const int kSingleCount_{prec} = {len(cfgs)};")
+    lines.append(f"extern const int kSingleCount_{prec}_{part} = {len(cfgs)};")
+    lines.append("}  // namespace tfft")
+    return "\n".join(lines) + "\n"
+
+
+SINGLE_PARTS = 4
+
+
+def _emit_single_index(parts):
+    lines = ["// GENERATED by paper_2405_02520_b200/codegen.py — do not edit.",
+             '#include "registry.h"', "namespace tfft {"]
+    for prec in ("fp32", "fp64"):
+        for p in range(parts):
+            lines.append(f"extern const SingleEntry kSingle_{prec}_{p}[];")
+            lines.append(f"extern const int kSingleCount_{prec}_{p};")
+        lines.append(f"const SingleTable kSingleTables_{prec}[] = {{"
+                     + ", ".join(f"{{kSingle_{prec}_{p}, &kSingleCount_{prec}_{p}}}"
+                                 for p in range(parts)) + "};")
+    lines.append(f"const int kSingleParts = {parts};")
     lines.append("}  // namespace tfft")
     return "\n".join(lines) + "\n"
 
@@ -151,14 +222,14 @@ PASS_TABLE = {
     "fp32": {
         1: (2, (2,), 16), 2: (4, (4,), 16), 3: (8, (8,), 16), 4: (16, (16,), 16),
         5: (8, (8, 4), 16), 6: (8, (8, 8), 16), 7: (16, (16, 8), 16),
-        8: (16, (16, 16), 16), 9: (16, (16, 16, 2), 16), 10: (16, (16, 16, 4), 16),
-        11: (16, (16, 16, 8), 8),
+        8: (16, (16, 16), 16), 9: (16, (16, 16, 2), 16), 10: (16, (16, 16, 4), 8),
+        11: (16, (16, 16, 8), 4),
     },
     "fp64": {
         1: (2, (2,), 8), 2: (4, (4,), 8), 3: (8, (8,), 8), 4: (16, (16,), 8),
         5: (8, (8, 4), 8), 6: (8, (8, 8), 8), 7: (16, (16, 8), 8),
-        8: (16, (16, 16), 8), 9: (16, (16, 16, 2), 8), 10: (16, (16, 16, 4), 8),
-        11: (16, (16, 16, 8), 4),
+        8: (16, (16, 16), 8), 9: (8, (8, 8, 8), 8), 10: (8, (8, 8, 8, 2), 8),
+        11: (8, (8, 8, 8, 4), 4),
     },
 }
 
@@ -253,11 +324,20 @@ def _write(path, text):
 def generate(verbose=False):
     cfgs = single_configs()
     written = []
+    for old in ("gen_single_fp32.cu", "gen_single_fp64.cu"):
+        if os.path.exists(os.path.join(CSRC, old)):
+            os.remove(os.path.join(CSRC, old))
+    path = os.path.join(CSRC, "gen_single_index.cu")
+    _write(path, _emit_single_index(SINGLE_PARTS))
+    written.append(path)
     for prec in ("fp32", "fp64"):
-        text = _emit_single(prec, [c for c in cfgs if c["prec"] == prec])
-        path = os.path.join(CSRC, f"gen_single_{prec}.cu")
-        _write(path, text)
-        written.append(path)
+        mine = [c for c in cfgs if c["prec"] == prec]
+        # round-robin by size so the parts compile in similar time
+        for p in range(SINGLE_PARTS):
+            part = [c for i, c in enumerate(mine) if c["logn"] % SINGLE_PARTS == p]
+            path = os.path.join(CSRC, f"gen_single_{prec}_{p}.cu")
+            _write(path, _emit_single(prec, part, p))
+            written.append(path)
         pcfgs = [c for c in pass_configs() if c["prec"] == prec]
         path = os.path.join(CSRC, f"gen_pass_{prec}.cu")
         _write(path, _emit_pass(prec, pcfgs))

@@ -5,16 +5,22 @@ namespace tfft {
 
 struct SingleEntry {
     int logn;
+    int variant;     // index into codegen.SINGLE_CANDIDATES[prec][logn]
+    int chosen;      // 1 for the tuned default
     int e;           // elements per thread
     int threads;     // CTA size
     int smem;        // dynamic shared memory bytes
     int tps;         // threads per signal
-    const void* fn[3];  // ABFT off / Wang / table
+    const void* fn[3];  // ABFT off / Wang / table (table only on the chosen variant)
 };
 
-extern const SingleEntry kSingle_fp32[];
-extern const int kSingleCount_fp32;
-extern const SingleEntry kSingle_fp64[];
-extern const int kSingleCount_fp64;
+struct SingleTable {
+    const SingleEntry* entries;
+    const int* count;
+};
+
+extern const SingleTable kSingleTables_fp32[];
+extern const SingleTable kSingleTables_fp64[];
+extern const int kSingleParts;
 
 }  // namespace tfft

@@ -75,25 +75,76 @@ __device__ __forceinline__ T sig_sum(T val, T* scratch, int t) {
     return val;
 }
 
-template <class T, int N, int E, int PS, int ABFT, int THREADS, class Radices>
-__global__ void __launch_bounds__(THREADS)
+// Smem slice length of one signal: the Stockham exchange buffer and/or the
+// staging buffer of coalesced I/O (stride N+1 keeps per-thread rows off the
+// same banks).
+template <int N, int PS, bool MULTIPASS, bool STAGE>
+struct SliceLen {
+    static constexpr int ex = MULTIPASS ? SmemLen<N, PS>::v : 0;
+    static constexpr int st = STAGE ? N + 1 : 0;
+    static constexpr int v = ex > st ? ex : st;
+};
+
+// CTA-cooperative, fully coalesced vector copies between HBM and the staging
+// slices (used when a signal is too short for per-thread coalescing).
+template <class T, int N, int S, int SL, int THREADS>
+__device__ __forceinline__ void stage_in(const C<T>* __restrict__ src, long long valid, C<T>* sm_all) {
+    if constexpr (sizeof(T) == 4) {
+        const float4* s4 = reinterpret_cast<const float4*>(src);
+        for (int i = threadIdx.x; i < S * N / 2; i += THREADS) {
+            const int e = 2 * i;
+            if (e < valid) {
+                const float4 q = __ldcs(s4 + i);
+                const int sg = e / N, p = e % N;
+                sm_all[sg * SL + p] = make_float2(q.x, q.y);
+                sm_all[sg * SL + p + 1] = make_float2(q.z, q.w);
+            }
+        }
+    } else {
+        for (int e = threadIdx.x; e < S * N; e += THREADS) {
+            if (e < valid) sm_all[(e / N) * SL + e % N] = __ldcs(src + e);
+        }
+    }
+}
+template <class T, int N, int S, int SL, int THREADS>
+__device__ __forceinline__ void stage_out(C<T>* __restrict__ dst, long long valid, const C<T>* sm_all) {
+    if constexpr (sizeof(T) == 4) {
+        float4* d4 = reinterpret_cast<float4*>(dst);
+        for (int i = threadIdx.x; i < S * N / 2; i += THREADS) {
+            const int e = 2 * i;
+            if (e < valid) {
+                const int sg = e / N, p = e % N;
+                const float2 u = sm_all[sg * SL + p], w = sm_all[sg * SL + p + 1];
+                __stcs(d4 + i, make_float4(u.x, u.y, w.x, w.y));
+            }
+        }
+    } else {
+        for (int e = threadIdx.x; e < S * N; e += THREADS) {
+            if (e < valid) __stcs(dst + e, sm_all[(e / N) * SL + e % N]);
+        }
+    }
+}
+
+template <class T, int N, int E, int PS, int ABFT, int THREADS, int MINB, int STAGE, class Radices>
+__global__ void __launch_bounds__(THREADS, MINB)
 fft_single_kernel(const SingleArgs<T> a) {
     using Eng = Engine<T, N, E, Radices>;
     constexpr int TPS = N / E;
     constexpr int S = THREADS / TPS;  // signals per CTA
     static_assert(S >= 1 && S * TPS == THREADS, "CTA must hold whole signals");
+    static_assert(!STAGE || N >= 2, "staging needs N >= 2");
     constexpr bool MULTIPASS = RCount<Radices>::v > 1;
-    constexpr int SLEN = MULTIPASS ? SmemLen<N, PS>::v : 0;
+    constexpr int SL = SliceLen<N, PS, MULTIPASS, STAGE != 0>::v;
     constexpr int NW = THREADS / 32 > 0 ? THREADS / 32 : 1;
 
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C<T>* sm_all = reinterpret_cast<C<T>*>(smem_raw);
-    T* red = reinterpret_cast<T*>(sm_all + S * SLEN);  // NW partial sums
+    T* red = reinterpret_cast<T*>(sm_all + S * SL);  // NW partial sums
     __shared__ typename KeyT<T>::type cta_max;
 
     const int sl = threadIdx.x / TPS;
     const int t = threadIdx.x % TPS;
-    C<T>* sm = sm_all + sl * SLEN;
+    C<T>* sm = sm_all + sl * SL;
     T my_max = T(0);
     if (threadIdx.x == 0) cta_max = 0;
 
@@ -103,9 +154,16 @@ fft_single_kernel(const SingleArgs<T> a) {
         const bool live = b < a.batch;
         const C<T>* src = a.in + b * N;
         C<T>* dst = a.out + b * N;
+        const long long valid = (a.batch - tile * S) * N;  // elements of this CTA chunk in range
 
         C<T> v[E];
-        if (live) {
+        if constexpr (STAGE) {
+            stage_in<T, N, S, SL, THREADS>(a.in + tile * S * N, valid, sm_all);
+            __syncthreads();
+#pragma unroll
+            for (int m = 0; m < E; ++m) v[m] = live ? sm[t + m * TPS] : mk<T>(T(0), T(0));
+            __syncthreads();
+        } else if (live) {
 #pragma unroll
             for (int m = 0; m < E; ++m) {
                 if constexpr (TPS >= 4) v[m] = __ldcs(src + t + m * TPS);
@@ -161,7 +219,13 @@ fft_single_kernel(const SingleArgs<T> a) {
         }
 
         // ---- store + output checksum
-        if (live) {
+        if constexpr (STAGE) {
+#pragma unroll
+            for (int m = 0; m < E; ++m) sm[t + m * TPS] = v[m];
+            __syncthreads();
+            stage_out<T, N, S, SL, THREADS>(a.out + tile * S * N, valid, sm_all);
+            __syncthreads();
+        } else if (live) {
 #pragma unroll
             for (int m = 0; m < E; ++m) {
                 if constexpr (TPS >= 4) __stcs(dst + t + m * TPS, v[m]);

@@ -93,12 +93,44 @@ struct Counters {
     unsigned long long max_key;  // float key in low 32 bits for fp32
 };
 
-const SingleEntry* single_entry(int prec, int logn) {
-    const SingleEntry* tab = prec == TFFT_FP32 ? kSingle_fp32 : kSingle_fp64;
-    const int cnt = prec == TFFT_FP32 ? kSingleCount_fp32 : kSingleCount_fp64;
-    for (int i = 0; i < cnt; ++i)
-        if (tab[i].logn == logn) return &tab[i];
-    return nullptr;
+// [prec][logn][variant] -> entry, plus the tuned default and a runtime override
+constexpr int kMaxVariants = 16;
+struct SingleIndex {
+    const SingleEntry* e[2][14][kMaxVariants] = {};
+    int count[2][14] = {};
+    int chosen[2][14] = {};
+    int override_[2][14];
+    SingleIndex() {
+        for (int p = 0; p < 2; ++p)
+            for (int l = 0; l < 14; ++l) override_[p][l] = -1;
+        for (int p = 0; p < 2; ++p) {
+            const SingleTable* tabs = p == TFFT_FP32 ? kSingleTables_fp32 : kSingleTables_fp64;
+            for (int part = 0; part < kSingleParts; ++part) {
+                for (int i = 0; i < *tabs[part].count; ++i) {
+                    const SingleEntry* en = &tabs[part].entries[i];
+                    if (en->logn < 0 || en->logn >= 14 || en->variant >= kMaxVariants) continue;
+                    e[p][en->logn][en->variant] = en;
+                    count[p][en->logn] = std::max(count[p][en->logn], en->variant + 1);
+                    if (en->chosen) chosen[p][en->logn] = en->variant;
+                }
+            }
+        }
+    }
+};
+SingleIndex& single_index() {
+    static SingleIndex idx;
+    return idx;
+}
+
+// The entry a launch uses: the runtime override (tuning) or the tuned default;
+// table encodings are only instantiated on the default variant.
+const SingleEntry* single_entry(int prec, int logn, int abft = 0) {
+    if (logn < 0 || logn >= 14) return nullptr;
+    SingleIndex& ix = single_index();
+    const int ov = ix.override_[prec][logn];
+    const SingleEntry* en = ix.e[prec][logn][ov >= 0 ? ov : ix.chosen[prec][logn]];
+    if (en && !en->fn[abft]) en = ix.e[prec][logn][ix.chosen[prec][logn]];
+    return en;
 }
 
 std::mutex g_attr_mu;
@@ -192,7 +224,8 @@ struct Launch {
 
 template <class T>
 int launch_single_t(tfft_plan* p, const Launch& L, cudaStream_t st) {
-    const SingleEntry* e = p->single;
+    const SingleEntry* e = single_entry(p->prec, p->logn, L.abft);
+    if (!e) return fail(TFFT_EUNSUPPORTED, "no single-kernel config");
     const void* fn = e->fn[L.abft];
     int nb = 0;
     int rc = prepare_kernel(fn, e->threads, e->smem, &nb);
@@ -278,6 +311,21 @@ int check_plan(tfft_plan* p) {
 extern "C" {
 
 const char* tfft_last_error(void) { return g_err.c_str(); }
+
+int tfft_tune_variants(int precision, int logn) {
+    if ((precision != TFFT_FP32 && precision != TFFT_FP64) || logn < 1 || logn > 13) return 0;
+    return single_index().count[precision][logn];
+}
+
+int tfft_tune_select(int precision, int logn, int variant) {
+    if ((precision != TFFT_FP32 && precision != TFFT_FP64) || logn < 1 || logn > 13)
+        return fail(TFFT_EINVAL, "no single-kernel size");
+    SingleIndex& ix = single_index();
+    if (variant >= ix.count[precision][logn] || (variant >= 0 && !ix.e[precision][logn][variant]))
+        return fail(TFFT_EINVAL, "no such variant");
+    ix.override_[precision][logn] = variant < 0 ? -1 : variant;
+    return TFFT_OK;
+}
 int tfft_version(void) { return 1; }
 
 int tfft_plan_create(tfft_plan** out, int64_t n, int precision, int nstages, const int64_t* dims,
