@@ -9,6 +9,7 @@
 // * in-register natural-order DFTs of size 2..64 built by template recursion.
 #pragma once
 #include <cstdint>
+#include <limits>
 #include <cuda_runtime.h>
 
 namespace tfft {

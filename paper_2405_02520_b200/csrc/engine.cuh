@@ -65,7 +65,8 @@ struct Engine {
     static_assert(RProd<Radices>::v == L, "radices must multiply to L");
     static_assert(E <= L && L % E == 0, "bad E");
 
-    // tw[k] = w_L^k (k < L) in T precision.
+    // tw: multi-resolution root table, tw[M + k] = w_M^k for every power of
+    // two M <= L and k < M (2L entries, see twiddle_table_size()).
     template <class Mem>
     static __device__ __forceinline__ void run(C<T> (&v)[E], const Mem& mem, int t,
                                                const C<T>* __restrict__ tw) {
@@ -73,6 +74,40 @@ struct Engine {
     }
 
   private:
+    // Pass twiddles w^r (r = 1..R-1, w = w_M^k, M = Ns*R): two contiguous
+    // lookups (w and w^Q, lanes read consecutive k) and binary powering for
+    // the rest, so a butterfly costs 2 loads instead of R-1 scattered ones
+    // (which made L1TEX the bottleneck) at <= ~3 ulp of extra error.
+    template <int Ns, int R, int SUB>
+    static __device__ __forceinline__ void twiddle(C<T> (&v)[E], int q, int k,
+                                                   const C<T>* __restrict__ tw) {
+        constexpr int M = Ns * R;
+        constexpr int Q = R <= 4 ? R : (R == 8 ? 4 : (R == 16 ? 4 : 8));
+        C<T> p[Q];  // p[b] = w^b, b < Q
+        p[1] = __ldg(tw + M + k);
+#pragma unroll
+        for (int b = 2; b < Q; ++b) p[b] = cmul<T>(p[b / 2], p[b - b / 2]);
+        if constexpr (Q == R) {
+#pragma unroll
+            for (int r = 1; r < R; ++r) v[q + r * SUB] = cmul<T>(v[q + r * SUB], p[r]);
+        } else {
+            constexpr int A = R / Q;
+            C<T> g[A];  // g[a] = w^(Q a)
+            g[1] = __ldg(tw + M / Q + k);
+#pragma unroll
+            for (int a = 2; a < A; ++a) g[a] = cmul<T>(g[a / 2], g[a - a / 2]);
+#pragma unroll
+            for (int r = 1; r < R; ++r) {
+                const int a = r / Q, b = r % Q;
+                C<T> w;
+                if (a == 0) w = p[b];
+                else if (b == 0) w = g[a];
+                else w = cmul<T>(g[a], p[b]);
+                v[q + r * SUB] = cmul<T>(v[q + r * SUB], w);
+            }
+        }
+    }
+
     template <int Ns, class Mem, int R, int... Rest>
     static __device__ __forceinline__ void passes(C<T> (&v)[E], const Mem& mem, int t,
                                                   const C<T>* __restrict__ tw,
@@ -82,16 +117,7 @@ struct Engine {
 #pragma unroll
         for (int q = 0; q < SUB; ++q) {
             const int j = t + q * TPS;
-            if constexpr (Ns > 1) {
-                // w_{Ns R}^{k r} = w_L^{k r L/(Ns R)}, k = j mod Ns
-                const int k = j & (Ns - 1);
-                constexpr int STEP = L / (Ns * R);
-#pragma unroll
-                for (int r = 1; r < R; ++r) {
-                    C<T> w = __ldg(tw + k * r * STEP);
-                    v[q + r * SUB] = cmul<T>(v[q + r * SUB], w);
-                }
-            }
+            if constexpr (Ns > 1) twiddle<Ns, R, SUB>(v, q, j & (Ns - 1), tw);  // w_{Ns R}^{(j mod Ns) r}
             C<T> a[R];
 #pragma unroll
             for (int r = 0; r < R; ++r) a[r] = v[q + r * SUB];

@@ -151,14 +151,21 @@ fft_pass_kernel(const PassArgs<T> a) {
         }
         Eng::run(v, mem, t, a.twL);
         if constexpr (KIND != KIND_LAST) {
-            // post twiddle w_M^{c k} with c = lo (column), k = t + m*TPS
+            // post twiddle w_M^{c k} with c = lo (column), k = t + m*TPS:
+            // base w^{c t} and step w^{c TPS} from the two-level table (4
+            // loads per thread), powers of the step by binary splitting.
+            const long long lmask = (1ll << a.ptw_shift) - 1;
+            const long long e0 = (lo * (long long)t) & a.ptw_mask;
+            const long long es = (lo * (long long)TPS) & a.ptw_mask;
+            const C<T> base = cmul<T>(__ldg(a.ptw_hi + (e0 >> a.ptw_shift)), __ldg(a.ptw_lo + (e0 & lmask)));
+            C<T> st[E];
+            st[0] = mk<T>(T(1), T(0));
+            if constexpr (E > 1) st[1] = cmul<T>(__ldg(a.ptw_hi + (es >> a.ptw_shift)), __ldg(a.ptw_lo + (es & lmask)));
 #pragma unroll
-            for (int m = 0; m < E; ++m) {
-                const long long e = (lo * (long long)(t + m * TPS)) & a.ptw_mask;
-                const C<T> w = cmul<T>(__ldg(a.ptw_hi + (e >> a.ptw_shift)),
-                                       __ldg(a.ptw_lo + (e & ((1ll << a.ptw_shift) - 1))));
-                v[m] = cmul<T>(v[m], w);
-            }
+            for (int m = 2; m < E; ++m) st[m] = cmul<T>(st[m / 2], st[m - m / 2]);
+            v[0] = cmul<T>(v[0], base);
+#pragma unroll
+            for (int m = 1; m < E; ++m) v[m] = cmul<T>(v[m], cmul<T>(base, st[m]));
         }
         if (a.inverse) {
 #pragma unroll

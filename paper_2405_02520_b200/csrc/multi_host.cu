@@ -86,6 +86,28 @@ int upload_roots(int prec, long long N, long long count, long long stride, void*
     return TFFT_OK;
 }
 
+// t[M + k] = w_M^k for all powers of two M <= L (the engine's pass twiddles)
+int upload_multires(int prec, long long L, void** dst) {
+    const size_t es = prec == TFFT_FP32 ? 8 : 16;
+    MCU(cudaMalloc(dst, 2 * L * es));
+    std::vector<unsigned char> h(2 * L * es, 0);
+    for (long long M = 1; M <= L; M *= 2) {
+        for (long long k = 0; k < M; ++k) {
+            long double re = 1.0L, im = 0.0L;
+            if (M >= 2) root(M, k, &re, &im);
+            if (prec == TFFT_FP32) {
+                float2 v = make_float2((float)re, (float)im);
+                memcpy(&h[(M + k) * es], &v, es);
+            } else {
+                double2 v = make_double2((double)re, (double)im);
+                memcpy(&h[(M + k) * es], &v, es);
+            }
+        }
+    }
+    MCU(cudaMemcpy(*dst, h.data(), 2 * L * es, cudaMemcpyHostToDevice));
+    return TFFT_OK;
+}
+
 const PassEntry* pass_entry(int prec, int logl) {
     const PassEntry* tab = prec == TFFT_FP32 ? kPass_fp32 : kPass_fp64;
     const int cnt = prec == TFFT_FP32 ? kPassCount_fp32 : kPassCount_fp64;
@@ -286,7 +308,7 @@ int multi_plan_init(MultiPlan& mp, long long n, int prec, int nst, const int64_t
         const int kind = k == 0 ? KIND_FIRST : (k == nst - 1 ? KIND_LAST : KIND_MID);
         const long long lo_count = kind == KIND_FIRST ? R0 : (kind == KIND_MID ? mp.d[2] : mp.d[0]);
         if (lo_count % mp.pe[k]->u) return merr(TFFT_EUNSUPPORTED, "stage split too narrow for the tile width");
-        int rc = upload_roots(prec, mp.d[k], mp.d[k], 1, &mp.twL[k]);
+        int rc = upload_multires(prec, mp.d[k], &mp.twL[k]);
         if (rc) return rc;
         if (kind != KIND_LAST) {
             const long long M = kind == KIND_FIRST ? n : mp.d[1] * mp.d[2];

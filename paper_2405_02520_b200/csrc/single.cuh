@@ -265,14 +265,32 @@ fft_single_kernel(const SingleArgs<T> a) {
             bool flagged = false;
             T rel = T(0);
             if (t == 0 && live) {
-                const C<T> cI = mk<T>(r0, r1);
-                const C<T> raw = mk<T>(fsub(r0, r2), fsub(r1, r3));
+                // squared screen: rel^2 = |raw|^2 / max(|c_in|, floor)^2 with no
+                // sqrt/hypot/div on the common path; anything near the
+                // threshold, non-finite or out of range takes the exact
+                // reference arithmetic (pipeline.py:116-121), so decisions match.
+                const T dx = fsub(r0, r2), dy = fsub(r1, r3);
+                const T raw2 = ffma(dx, dx, fmul(dy, dy));
+                const T cin2 = ffma(r0, r0, fmul(r1, r1));
                 const T fl = nanmax<T>(a.abs_floor, fmul(a.floor_coef, r4));
-                const T den = nanmax<T>(cabs<T>(cI), fl);
-                rel = cabs<T>(raw) / den;
-                if (!isfinite(rel)) rel = T(INFINITY);
-                flagged = rel > a.delta;
-                my_max = my_max > rel ? my_max : rel;
+                const T den2 = nanmax<T>(cin2, fmul(fl, fl));
+                const T q = raw2 / den2;
+                const T d2 = fmul(a.delta, a.delta);
+                const bool in_range = den2 >= std::numeric_limits<T>::min() &&
+                                      den2 <= std::numeric_limits<T>::max() &&
+                                      raw2 <= std::numeric_limits<T>::max();
+                T rel2;
+                if (in_range && q < T(0.81) * d2) {
+                    rel2 = q;
+                    if (a.rel_out) rel = sqrt(q);
+                } else {
+                    const T den = nanmax<T>(cabs<T>(mk<T>(r0, r1)), fl);
+                    rel = cabs<T>(mk<T>(dx, dy)) / den;
+                    if (!isfinite(rel)) rel = T(INFINITY);
+                    flagged = rel > a.delta;
+                    rel2 = rel * rel;
+                }
+                my_max = my_max > rel2 ? my_max : rel2;  // squared; sqrt once per CTA
                 if (a.rel_out) a.rel_out[b] = rel;
             }
             // warp-aggregated append of flagged signals (rare)
@@ -294,7 +312,7 @@ fft_single_kernel(const SingleArgs<T> a) {
     }
     if constexpr (ABFT != ABFT_OFF) {
         // one atomic per CTA for the running max discrepancy
-        typename KeyT<T>::type k = order_key(my_max);
+        typename KeyT<T>::type k = order_key(sqrt(my_max));
 #pragma unroll
         for (int off = 16; off >= 1; off >>= 1) {
             typename KeyT<T>::type o = __shfl_xor_sync(0xffffffffu, k, off);

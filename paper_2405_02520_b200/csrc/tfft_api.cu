@@ -75,14 +75,20 @@ void unit_root(int64_t N, int64_t k, long double* re, long double* im) {
     *im = -s;
 }
 
+// Multi-resolution root table of the Stockham engine: t[M + k] = w_M^k for
+// every power of two 2 <= M <= L and k < M (engine.cuh), exactly rounded.
 template <class T>
-std::vector<C<T>> root_table(int64_t N, int64_t count, int64_t stride) {
-    std::vector<C<T>> t(count);
-    for (int64_t k = 0; k < count; ++k) {
-        long double re, im;
-        unit_root(N, k * stride, &re, &im);
-        t[k].x = (T)re;
-        t[k].y = (T)im;
+std::vector<C<T>> multires_table(int64_t L) {
+    std::vector<C<T>> t(2 * L);
+    t[0].x = t[1].x = (T)1;
+    t[0].y = t[1].y = (T)0;
+    for (int64_t M = 2; M <= L; M *= 2) {
+        for (int64_t k = 0; k < M; ++k) {
+            long double re, im;
+            unit_root(M, k, &re, &im);
+            t[M + k].x = (T)re;
+            t[M + k].y = (T)im;
+        }
     }
     return t;
 }
@@ -362,14 +368,14 @@ int tfft_plan_create(tfft_plan** out, int64_t n, int precision, int nstages, con
     if (p->logn <= 13) {
         p->single = single_entry(precision, p->logn);
         if (!p->single) return cleanup(fail(TFFT_EUNSUPPORTED, "no single-kernel config"));
-        size_t bytes = (size_t)n * p->esize;
+        size_t bytes = (size_t)2 * n * p->esize;
         if (cudaMalloc(&p->tw, bytes) != cudaSuccess) return cleanup(fail(TFFT_ENOMEM, "twiddle alloc"));
         cudaError_t ce;
         if (precision == TFFT_FP32) {
-            auto t = root_table<float>(n, n, 1);
+            auto t = multires_table<float>(n);
             ce = cudaMemcpy(p->tw, t.data(), bytes, cudaMemcpyHostToDevice);
         } else {
-            auto t = root_table<double>(n, n, 1);
+            auto t = multires_table<double>(n);
             ce = cudaMemcpy(p->tw, t.data(), bytes, cudaMemcpyHostToDevice);
         }
         if (ce != cudaSuccess) return cleanup(fail(TFFT_ECUDA, cudaGetErrorString(ce)));
