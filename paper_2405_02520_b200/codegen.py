@@ -166,7 +166,7 @@ def single_configs(all_candidates=True):
                 s = threads // tps
                 ex = (n + (n >> ps) + 1 if ps else n) if len(radices) > 1 else 0
                 st = n + 1 if c["stage"] else 0
-                smem = s * max(ex, st) * ELEM_BYTES[prec] + (threads // 32 + 1) * (ELEM_BYTES[prec] // 2)
+                smem = s * max(ex, st) * ELEM_BYTES[prec] + 5 * (threads // 32 + 1) * (ELEM_BYTES[prec] // 2)
                 out.append(dict(prec=prec, logn=logn, n=n, e=e, radices=radices, threads=threads,
                                 ps=ps, smem=smem, tps=tps, minb=c["minb"], stage=c["stage"],
                                 variant=vi, chosen=vi == chosen))
@@ -283,7 +283,7 @@ def pass_configs():
             assert threads <= 1024
             best = min((tile_cost(l, e, radices, u, p, eb), p) for p in (1, 0, 2, 3, 4, 5, 8))
             p = best[1]
-            smem = l * (u + p) * eb + (threads // 32 + 1) * (eb // 2)
+            smem = l * (u + p) * eb + 3 * (threads // 32 + 1) * (eb // 2)
             out.append(dict(prec=prec, logl=logl, l=l, e=e, radices=radices, u=u, p=p,
                             threads=threads, smem=smem))
     return out

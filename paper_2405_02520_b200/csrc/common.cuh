@@ -46,6 +46,88 @@ template <class T> __device__ __forceinline__ C<T> cmulc(C<T> a, C<T> b) {
 template <class T> __device__ __forceinline__ C<T> swapri(C<T> a) { return mk<T>(a.y, a.x); }
 template <class T> __device__ __forceinline__ C<T> cscale(C<T> a, T s) { return mk<T>(fmul(a.x, s), fmul(a.y, s)); }
 
+// ---- fp32: Blackwell packed f32x2 arithmetic (SASS FADD2/FMUL2/FFMA2).
+// A complex64 value is one 64-bit register pair, so complex add/sub is one
+// instruction and a multiply by a twiddle two (plus operand swizzles that
+// ptxas folds into the instruction). Every lane is still one IEEE rn op, and
+// the rounding sequence of each component is fixed, so all instantiations
+// stay bitwise consistent.
+namespace f2 {
+typedef unsigned long long u64;
+__device__ __forceinline__ u64 pk(float x, float y) {
+    u64 r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(x), "f"(y));
+    return r;
+}
+__device__ __forceinline__ float2 up(u64 r) {
+    float2 a;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a.x), "=f"(a.y) : "l"(r));
+    return a;
+}
+__device__ __forceinline__ u64 add(u64 a, u64 b) {
+    u64 r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ u64 sub(u64 a, u64 b) {
+    u64 r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ u64 mul(u64 a, u64 b) {
+    u64 r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ u64 fma(u64 a, u64 b, u64 c) {
+    u64 r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+}  // namespace f2
+
+template <> __device__ __forceinline__ float2 cadd<float>(float2 a, float2 b) {
+    return f2::up(f2::add(f2::pk(a.x, a.y), f2::pk(b.x, b.y)));
+}
+template <> __device__ __forceinline__ float2 csub<float>(float2 a, float2 b) {
+    return f2::up(f2::sub(f2::pk(a.x, a.y), f2::pk(b.x, b.y)));
+}
+// (ax wx - ay wy, ay wx + ax wy) = (a.x,a.y)*wx + (a.y,a.x)*(-wy, wy)
+template <> __device__ __forceinline__ float2 cmul<float>(float2 a, float2 w) {
+    return f2::up(f2::fma(f2::pk(a.x, a.y), f2::pk(w.x, w.x),
+                          f2::mul(f2::pk(a.y, a.x), f2::pk(-w.y, w.y))));
+}
+// a * conj(w) = (ax wx + ay wy, ay wx - ax wy)
+template <> __device__ __forceinline__ float2 cmulc<float>(float2 a, float2 w) {
+    return f2::up(f2::fma(f2::pk(a.x, a.y), f2::pk(w.x, w.x),
+                          f2::mul(f2::pk(a.y, a.x), f2::pk(w.y, -w.y))));
+}
+template <> __device__ __forceinline__ float2 cscale<float>(float2 a, float s) {
+    return f2::up(f2::mul(f2::pk(a.x, a.y), f2::pk(s, s)));
+}
+
+// a + (-i) b = (a.x + b.y, a.y - b.x) and a - (-i) b, one packed FMA each.
+template <class T> __device__ __forceinline__ C<T> add_mi(C<T> a, C<T> b) {
+    return mk<T>(fadd(a.x, b.y), fsub(a.y, b.x));
+}
+template <class T> __device__ __forceinline__ C<T> sub_mi(C<T> a, C<T> b) {
+    return mk<T>(fsub(a.x, b.y), fadd(a.y, b.x));
+}
+template <> __device__ __forceinline__ float2 add_mi<float>(float2 a, float2 b) {
+    return f2::up(f2::fma(f2::pk(b.y, b.x), f2::pk(1.0f, -1.0f), f2::pk(a.x, a.y)));
+}
+template <> __device__ __forceinline__ float2 sub_mi<float>(float2 a, float2 b) {
+    return f2::up(f2::fma(f2::pk(b.y, b.x), f2::pk(-1.0f, 1.0f), f2::pk(a.x, a.y)));
+}
+// acc + v * e  (ABFT dot-product step)
+template <class T> __device__ __forceinline__ C<T> cmac(C<T> acc, C<T> v, C<T> e) {
+    return mk<T>(ffma(v.x, e.x, ffma(-v.y, e.y, acc.x)), ffma(v.x, e.y, ffma(v.y, e.x, acc.y)));
+}
+template <> __device__ __forceinline__ float2 cmac<float>(float2 acc, float2 v, float2 e) {
+    const f2::u64 t = f2::fma(f2::pk(v.y, v.x), f2::pk(-e.y, e.y), f2::pk(acc.x, acc.y));
+    return f2::up(f2::fma(f2::pk(v.x, v.y), f2::pk(e.x, e.x), t));
+}
+
 // ---------------------------------------------------------------- constants
 // First octant of the 64th roots of unity: (cos, sin)(2*pi*k/64), k = 0..8.
 struct Oct { double c, s; };
@@ -82,16 +164,32 @@ __device__ __forceinline__ C<T> mul_w(C<T> z) {
         return mk<T>(-z.y, z.x);
     } else if constexpr (8 * m == R) {          // (1 - i)/sqrt2
         constexpr T h = T(0.7071067811865475244008444);
-        return mk<T>(fmul(fadd(z.x, z.y), h), fmul(fsub(z.y, z.x), h));
+        if constexpr (sizeof(T) == 4)
+            return f2::up(f2::mul(f2::fma(f2::pk(z.x, z.x), f2::pk(1.f, -1.f), f2::pk(z.y, z.y)),
+                                  f2::pk(h, h)));
+        else
+            return mk<T>(fmul(fadd(z.x, z.y), h), fmul(fsub(z.y, z.x), h));
     } else if constexpr (8 * m == 3 * R) {      // (-1 - i)/sqrt2
         constexpr T h = T(0.7071067811865475244008444);
-        return mk<T>(fmul(fsub(z.y, z.x), h), -fmul(fadd(z.x, z.y), h));
+        if constexpr (sizeof(T) == 4)
+            return f2::up(f2::mul(f2::fma(f2::pk(z.x, z.x), f2::pk(-1.f, 1.f), f2::pk(z.y, z.y)),
+                                  f2::pk(h, -h)));
+        else
+            return mk<T>(fmul(fsub(z.y, z.x), h), -fmul(fadd(z.x, z.y), h));
     } else if constexpr (8 * m == 5 * R) {      // (-1 + i)/sqrt2
         constexpr T h = T(0.7071067811865475244008444);
-        return mk<T>(-fmul(fadd(z.x, z.y), h), fmul(fsub(z.x, z.y), h));
+        if constexpr (sizeof(T) == 4)
+            return f2::up(f2::mul(f2::fma(f2::pk(z.y, z.y), f2::pk(1.f, -1.f), f2::pk(z.x, z.x)),
+                                  f2::pk(-h, h)));
+        else
+            return mk<T>(-fmul(fadd(z.x, z.y), h), fmul(fsub(z.x, z.y), h));
     } else if constexpr (8 * m == 7 * R) {      // (1 + i)/sqrt2
         constexpr T h = T(0.7071067811865475244008444);
-        return mk<T>(fmul(fsub(z.x, z.y), h), fmul(fadd(z.x, z.y), h));
+        if constexpr (sizeof(T) == 4)
+            return f2::up(f2::mul(f2::fma(f2::pk(z.y, z.y), f2::pk(-1.f, 1.f), f2::pk(z.x, z.x)),
+                                  f2::pk(h, h)));
+        else
+            return mk<T>(fmul(fsub(z.x, z.y), h), fmul(fadd(z.x, z.y), h));
     } else {
         static_assert(64 % R == 0, "compile-time twiddles limited to R <= 64");
         constexpr Oct u = unit64(m * (64 / R));
@@ -119,11 +217,10 @@ template <class T> struct Dft<T, 4> {
     static __device__ __forceinline__ void run(C<T>* a) {
         C<T> t0 = cadd<T>(a[0], a[2]), t1 = csub<T>(a[0], a[2]);
         C<T> t2 = cadd<T>(a[1], a[3]), d = csub<T>(a[1], a[3]);
-        C<T> t3 = mk<T>(d.y, -d.x);  // (a1 - a3) * (-i)
         a[0] = cadd<T>(t0, t2);
         a[2] = csub<T>(t0, t2);
-        a[1] = cadd<T>(t1, t3);
-        a[3] = csub<T>(t1, t3);
+        a[1] = add_mi<T>(t1, d);  // t1 + (a1 - a3)(-i)
+        a[3] = sub_mi<T>(t1, d);
     }
 };
 

@@ -49,19 +49,28 @@ struct PassArgs {
     int f_idx, f_where, f_comp, f_bit;  // f_where: 1 after load, 2 store pre-scale, 3 post-scale
 };
 
-template <class T>
-__device__ __forceinline__ T block_reduce_sum(T v, T* sh, int nwarps) {
+// K block-wide sums in one barrier round (thread 0 gets the totals). The
+// caller guarantees a barrier before `sh` is written again.
+template <int K, class T>
+__device__ __forceinline__ void block_reduce(T (&v)[K], T* sh, int nwarps) {
 #pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) v = fadd(v, shfl_xor(v, off));
-    __syncthreads();
-    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
-    __syncthreads();
-    T s = T(0);
-    if (threadIdx.x == 0) {
-        s = sh[0];
-        for (int w = 1; w < nwarps; ++w) s = fadd(s, sh[w]);
+    for (int off = 16; off >= 1; off >>= 1) {
+#pragma unroll
+        for (int i = 0; i < K; ++i) v[i] = fadd(v[i], shfl_xor(v[i], off));
     }
-    return s;
+    if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+        for (int i = 0; i < K; ++i) sh[(threadIdx.x >> 5) * K + i] = v[i];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int i = 0; i < K; ++i) {
+            T s = sh[i];
+            for (int w = 1; w < nwarps; ++w) s = fadd(s, sh[w * K + i]);
+            v[i] = s;
+        }
+    }
 }
 
 template <class T, int L, int E, int U, int P, int KIND, int ABFT, class Radices>
@@ -128,16 +137,14 @@ fft_pass_kernel(const PassArgs<T> a) {
 #pragma unroll
             for (int m = 0; m < E; ++m) {
                 const C<T> e = __ldg(a.etw + ibase + (long long)(t + m * TPS) * a.in_j);
-                cin.x = ffma(v[m].x, e.x, ffma(-v[m].y, e.y, cin.x));
-                cin.y = ffma(v[m].x, e.y, ffma(v[m].y, e.x, cin.y));
+                cin = cmac<T>(cin, v[m], e);
                 l1 = fadd(l1, mag_fast(v[m]));
             }
-            T s0 = block_reduce_sum(cin.x, red, THREADS / 32);
-            T s1 = block_reduce_sum(cin.y, red, THREADS / 32);
-            T s2 = block_reduce_sum(l1, red, THREADS / 32);
+            T s[3] = {cin.x, cin.y, l1};
+            block_reduce<3>(s, red, THREADS / 32);
             if (threadIdx.x == 0) {
                 T* p = a.part + tix * 3;
-                p[0] = s0; p[1] = s1; p[2] = s2;
+                p[0] = s[0]; p[1] = s[1]; p[2] = s[2];
             }
         }
         if (fsig && a.f_where == 1) {
@@ -203,11 +210,11 @@ fft_pass_kernel(const PassArgs<T> a) {
                 }
                 cout = cadd<T>(cout, cmul<T>(v[m], e));
             }
-            T s0 = block_reduce_sum(cout.x, red, THREADS / 32);
-            T s1 = block_reduce_sum(cout.y, red, THREADS / 32);
+            T s[2] = {cout.x, cout.y};
+            block_reduce<2>(s, red, THREADS / 32);
             if (threadIdx.x == 0) {
                 T* p = a.part + tix * 2;
-                p[0] = s0; p[1] = s1;
+                p[0] = s[0]; p[1] = s[1];
             }
         }
         __syncthreads();  // smem tile reused by the next iteration

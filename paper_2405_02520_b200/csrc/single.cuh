@@ -52,27 +52,36 @@ template <class T> __device__ __forceinline__ T nanmax(T a, T b) {
     return (a != a) ? a : ((b != b) ? b : (a > b ? a : b));
 }
 
-// Sum `val` over the TPS consecutive threads of one signal (deterministic
-// tree). For TPS > 32 the per-warp partials go through `scratch` (one slot
-// per warp of the CTA); only thread t == 0 of the signal gets the total.
-template <int TPS, class T>
-__device__ __forceinline__ T sig_sum(T val, T* scratch, int t) {
+// Sum K values over the TPS consecutive threads of one signal (deterministic
+// tree). For TPS > 32 the per-warp partials go through `scratch` (K slots per
+// warp of the CTA) with a single barrier; only thread t == 0 of the signal
+// gets the totals. The scratch is next written only after the following
+// tile's Stockham barriers, so no trailing barrier is needed.
+template <int TPS, int K, class T>
+__device__ __forceinline__ void sig_sum(T (&val)[K], T* scratch, int t) {
     constexpr int W = TPS < 32 ? TPS : 32;
 #pragma unroll
-    for (int off = W / 2; off >= 1; off >>= 1) val = fadd(val, shfl_xor(val, off));
+    for (int off = W / 2; off >= 1; off >>= 1) {
+#pragma unroll
+        for (int i = 0; i < K; ++i) val[i] = fadd(val[i], shfl_xor(val[i], off));
+    }
     if constexpr (TPS > 32) {
         const int warp = threadIdx.x >> 5;
-        __syncthreads();
-        if ((threadIdx.x & 31) == 0) scratch[warp] = val;
+        if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+            for (int i = 0; i < K; ++i) scratch[warp * K + i] = val[i];
+        }
         __syncthreads();
         if (t == 0) {
-            T s = scratch[warp];
 #pragma unroll
-            for (int w = 1; w < TPS / 32; ++w) s = fadd(s, scratch[warp + w]);
-            val = s;
+            for (int i = 0; i < K; ++i) {
+                T s = scratch[warp * K + i];
+#pragma unroll
+                for (int w = 1; w < TPS / 32; ++w) s = fadd(s, scratch[(warp + w) * K + i]);
+                val[i] = s;
+            }
         }
     }
-    return val;
 }
 
 // Smem slice length of one signal: the Stockham exchange buffer and/or the
@@ -139,7 +148,7 @@ fft_single_kernel(const SingleArgs<T> a) {
 
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C<T>* sm_all = reinterpret_cast<C<T>*>(smem_raw);
-    T* red = reinterpret_cast<T*>(sm_all + S * SL);  // NW partial sums
+    T* red = reinterpret_cast<T*>(sm_all + S * SL);  // 5 partial sums per warp
     __shared__ typename KeyT<T>::type cta_max;
 
     const int sl = threadIdx.x / TPS;
@@ -181,8 +190,7 @@ fft_single_kernel(const SingleArgs<T> a) {
 #pragma unroll
             for (int m = 0; m < E; ++m) {
                 const C<T> e = __ldg(a.etw + t + m * TPS);
-                cin.x = ffma(v[m].x, e.x, ffma(-v[m].y, e.y, cin.x));
-                cin.y = ffma(v[m].x, e.y, ffma(v[m].y, e.x, cin.y));
+                cin = cmac<T>(cin, v[m], e);
                 l1 = fadd(l1, mag_fast(v[m]));
             }
         }
@@ -257,11 +265,9 @@ fft_single_kernel(const SingleArgs<T> a) {
                     cout = cadd<T>(cout, cmul<T>(v[m], e));
                 }
             }
-            T r0 = sig_sum<TPS>(cin.x, red, t);
-            T r1 = sig_sum<TPS>(cin.y, red, t);
-            T r2 = sig_sum<TPS>(cout.x, red, t);
-            T r3 = sig_sum<TPS>(cout.y, red, t);
-            T r4 = sig_sum<TPS>(l1, red, t);
+            T sums[5] = {cin.x, cin.y, cout.x, cout.y, l1};
+            sig_sum<TPS>(sums, red, t);
+            const T r0 = sums[0], r1 = sums[1], r2 = sums[2], r3 = sums[3], r4 = sums[4];
             bool flagged = false;
             T rel = T(0);
             if (t == 0 && live) {
