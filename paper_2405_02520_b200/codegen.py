@@ -40,20 +40,25 @@ SINGLE_CANDIDATES = {
         6: _cands((8, (8, 8), 256, 1, 1), (8, (8, 8), 256, 1, 0), (16, (16, 4), 256, 1, 1),
                   (16, (16, 4), 256, 1, 0)),
         7: _cands((16, (16, 8), 256, 1, 0), (16, (16, 8), 256, 1, 1), (8, (8, 8, 2), 256, 1, 0),
-                  (16, (16, 8), 256, 3, 0)),
+                  (16, (16, 8), 256, 3, 0), (16, (16, 8), 256, 1, 2)),
         8: _cands((16, (16, 16), 256, 1, 0), (16, (16, 16), 256, 3, 0), (8, (8, 8, 4), 256, 1, 0),
-                  (16, (16, 16), 256, 1, 1)),
+                  (16, (16, 16), 256, 1, 1), (16, (16, 16), 256, 1, 2), (16, (16, 16), 256, 3, 2)),
         9: _cands((16, (16, 16, 2), 256, 2, 0), (32, (32, 16), 256, 1, 0),
-                  (8, (8, 8, 8), 256, 3, 0), (16, (16, 16, 2), 256, 3, 0)),
+                  (8, (8, 8, 8), 256, 3, 0), (16, (16, 16, 2), 256, 3, 0),
+                  (16, (16, 16, 2), 256, 2, 2), (8, (8, 8, 8), 256, 3, 2)),
         10: _cands((16, (16, 16, 4), 256, 2, 0), (32, (32, 32), 256, 1, 0),
                    (16, (16, 16, 4), 256, 3, 0), (8, (8, 8, 8, 2), 256, 2, 0),
-                   (16, (16, 16, 4), 512, 1, 0)),
+                   (16, (16, 16, 4), 512, 1, 0), (16, (16, 16, 4), 256, 3, 2),
+                   (16, (16, 16, 4), 256, 2, 2)),
         11: _cands((16, (16, 16, 8), 256, 2, 0), (16, (16, 16, 8), 256, 3, 0),
-                   (8, (8, 8, 8, 4), 256, 3, 0), (16, (16, 16, 8), 512, 1, 0)),
+                   (8, (8, 8, 8, 4), 256, 3, 0), (16, (16, 16, 8), 512, 1, 0),
+                   (16, (16, 16, 8), 256, 3, 2), (16, (16, 16, 8), 256, 2, 2)),
         12: _cands((16, (16, 16, 16), 256, 2, 0), (16, (16, 16, 16), 256, 3, 0),
-                   (8, (8, 8, 8, 8), 512, 2, 0), (16, (16, 16, 16), 512, 1, 0)),
+                   (8, (8, 8, 8, 8), 512, 2, 0), (16, (16, 16, 16), 512, 1, 0),
+                   (16, (16, 16, 16), 256, 3, 2), (16, (16, 16, 16), 256, 2, 2)),
         13: _cands((16, (16, 16, 16, 2), 512, 2, 0), (32, (32, 16, 16), 256, 1, 0),
-                   (16, (16, 16, 16, 2), 512, 1, 0), (8, (8, 8, 8, 8, 2), 1024, 1, 0)),
+                   (16, (16, 16, 16, 2), 512, 1, 0), (8, (8, 8, 8, 8, 2), 1024, 1, 0),
+                   (16, (16, 16, 16, 2), 512, 2, 2), (16, (16, 16, 16, 2), 512, 1, 2)),
     },
     "fp64": {
         1: _cands((2, (2,), 256, 1, 1), (2, (2,), 256, 1, 0)),
@@ -62,16 +67,18 @@ SINGLE_CANDIDATES = {
         4: _cands((16, (16,), 256, 1, 1), (8, (8, 2), 256, 1, 1), (4, (4, 4), 256, 1, 1)),
         5: _cands((8, (8, 4), 256, 1, 1), (8, (8, 4), 256, 1, 0), (16, (16, 2), 256, 1, 1)),
         6: _cands((8, (8, 8), 256, 1, 1), (8, (8, 8), 256, 1, 0), (16, (16, 4), 256, 1, 0)),
-        7: _cands((16, (16, 8), 256, 1, 0), (8, (8, 8, 2), 256, 1, 0), (16, (16, 8), 256, 1, 1)),
-        8: _cands((16, (16, 16), 256, 1, 0), (8, (8, 8, 4), 256, 1, 0), (16, (16, 16), 256, 2, 0)),
+        7: _cands((16, (16, 8), 256, 1, 0), (8, (8, 8, 2), 256, 1, 0), (16, (16, 8), 256, 1, 1),
+                  (16, (16, 8), 256, 1, 2)),
+        8: _cands((16, (16, 16), 256, 1, 0), (8, (8, 8, 4), 256, 1, 0), (16, (16, 16), 256, 2, 0),
+                  (16, (16, 16), 256, 2, 2)),
         9: _cands((8, (8, 8, 8), 256, 1, 0), (16, (16, 16, 2), 256, 1, 0),
-                  (8, (8, 8, 8), 256, 3, 0)),
+                  (8, (8, 8, 8), 256, 3, 0), (8, (8, 8, 8), 256, 3, 2)),
         10: _cands((16, (16, 16, 4), 256, 1, 0), (8, (8, 8, 8, 2), 256, 1, 0),
-                   (16, (16, 16, 4), 256, 2, 0)),
+                   (16, (16, 16, 4), 256, 2, 0), (16, (16, 16, 4), 256, 2, 2)),
         11: _cands((16, (16, 16, 8), 256, 1, 0), (16, (16, 16, 8), 256, 2, 0),
-                   (8, (8, 8, 8, 4), 256, 2, 0)),
+                   (8, (8, 8, 8, 4), 256, 2, 0), (16, (16, 16, 8), 256, 2, 2)),
         12: _cands((16, (16, 16, 16), 256, 1, 0), (16, (16, 16, 16), 512, 1, 0),
-                   (8, (8, 8, 8, 8), 512, 1, 0)),
+                   (8, (8, 8, 8, 8), 512, 1, 0), (16, (16, 16, 16), 256, 1, 2)),
         13: _cands((16, (16, 16, 16, 2), 512, 1, 0), (8, (8, 8, 8, 8, 2), 1024, 1, 0)),
     },
 }
@@ -165,8 +172,10 @@ def single_configs(all_candidates=True):
                 ps, _ = choose_padding(n, e, radices, prec)
                 s = threads // tps
                 ex = (n + (n >> ps) + 1 if ps else n) if len(radices) > 1 else 0
-                st = n + 1 if c["stage"] else 0
-                smem = s * max(ex, st) * ELEM_BYTES[prec] + 5 * (threads // 32 + 1) * (ELEM_BYTES[prec] // 2)
+                st = n + 1 if c["stage"] == 1 else 0
+                ib = s * n if c["stage"] == 2 else 0  # TMA prefetch buffer
+                smem = ((ib + s * max(ex, st)) * ELEM_BYTES[prec]
+                        + 5 * (threads // 32 + 1) * (ELEM_BYTES[prec] // 2))
                 out.append(dict(prec=prec, logn=logn, n=n, e=e, radices=radices, threads=threads,
                                 ps=ps, smem=smem, tps=tps, minb=c["minb"], stage=c["stage"],
                                 variant=vi, chosen=vi == chosen))

@@ -80,7 +80,7 @@ fft_pass_kernel(const PassArgs<T> a) {
     constexpr int THREADS = U * TPS;
     constexpr int RS = U + P;  // smem row stride (elements) of the [L][U] tile
     using Eng = Engine<T, L, E, Radices>;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     C<T>* tile = reinterpret_cast<C<T>*>(smem_raw);
     T* red = reinterpret_cast<T*>(tile + L * RS);
 

@@ -142,14 +142,21 @@ fft_single_kernel(const SingleArgs<T> a) {
     constexpr int S = THREADS / TPS;  // signals per CTA
     static_assert(S >= 1 && S * TPS == THREADS, "CTA must hold whole signals");
     static_assert(!STAGE || N >= 2, "staging needs N >= 2");
+    // STAGE: 0 direct coalesced loads, 1 CTA-staged vector I/O (short
+    // signals), 2 TMA bulk prefetch of the next tile into smem (cp.async.bulk
+    // + mbarrier) while the current tile computes.
+    constexpr bool STG = STAGE == 1;
+    constexpr bool PF = STAGE == 2;
     constexpr bool MULTIPASS = RCount<Radices>::v > 1;
-    constexpr int SL = SliceLen<N, PS, MULTIPASS, STAGE != 0>::v;
+    constexpr int SL = SliceLen<N, PS, MULTIPASS, STG>::v;
     constexpr int NW = THREADS / 32 > 0 ? THREADS / 32 : 1;
 
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    C<T>* sm_all = reinterpret_cast<C<T>*>(smem_raw);
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    C<T>* ib = reinterpret_cast<C<T>*>(smem_raw);  // prefetch buffer (PF)
+    C<T>* sm_all = ib + (PF ? S * N : 0);
     T* red = reinterpret_cast<T*>(sm_all + S * SL);  // 5 partial sums per warp
     __shared__ typename KeyT<T>::type cta_max;
+    __shared__ unsigned long long in_bar;
 
     const int sl = threadIdx.x / TPS;
     const int t = threadIdx.x % TPS;
@@ -158,7 +165,19 @@ fft_single_kernel(const SingleArgs<T> a) {
     if (threadIdx.x == 0) cta_max = 0;
 
     const long long tiles = (a.batch + S - 1) / S;
-    for (long long tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    auto prefetch = [&](long long tl) {  // thread 0 only
+        const long long nsig = (a.batch - tl * S) < S ? (a.batch - tl * S) : S;
+        const unsigned bytes = (unsigned)(nsig * N * sizeof(C<T>));
+        mbar_expect_tx(&in_bar, bytes);
+        bulk_g2s(ib, a.in + tl * S * N, bytes, &in_bar);
+    };
+    if constexpr (PF) {
+        if (threadIdx.x == 0) mbar_init(&in_bar, 1);
+        __syncthreads();
+        if (threadIdx.x == 0 && blockIdx.x < tiles) prefetch(blockIdx.x);
+    }
+    unsigned iter = 0;
+    for (long long tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++iter) {
         const long long b = tile * S + sl;
         const bool live = b < a.batch;
         const C<T>* src = a.in + b * N;
@@ -166,7 +185,16 @@ fft_single_kernel(const SingleArgs<T> a) {
         const long long valid = (a.batch - tile * S) * N;  // elements of this CTA chunk in range
 
         C<T> v[E];
-        if constexpr (STAGE) {
+        if constexpr (PF) {
+            mbar_wait(&in_bar, iter & 1);
+#pragma unroll
+            for (int m = 0; m < E; ++m) v[m] = live ? ib[sl * N + t + m * TPS] : mk<T>(T(0), T(0));
+            __syncthreads();  // everyone has the tile in registers: refill the buffer
+            if (threadIdx.x == 0 && tile + gridDim.x < tiles) {
+                fence_proxy_async();
+                prefetch(tile + gridDim.x);
+            }
+        } else if constexpr (STG) {
             stage_in<T, N, S, SL, THREADS>(a.in + tile * S * N, valid, sm_all);
             __syncthreads();
 #pragma unroll
@@ -227,7 +255,7 @@ fft_single_kernel(const SingleArgs<T> a) {
         }
 
         // ---- store + output checksum
-        if constexpr (STAGE) {
+        if constexpr (STG) {
 #pragma unroll
             for (int m = 0; m < E; ++m) sm[t + m * TPS] = v[m];
             __syncthreads();
