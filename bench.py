@@ -54,7 +54,7 @@ class ClockSampler:
     """Samples SM clocks and throttle reasons through NVML every 50 ms while
     the timed region runs (the recipe's nvidia-smi clocks line, in-process)."""
 
-    def __init__(self, index, period=0.05):
+    def __init__(self, index, period=0.005):
         self.index = index
         self.period = period
         self.samples = []
@@ -418,7 +418,7 @@ def run_reference(args, rank, world):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--skip-cpu", action="store_true", help="skip the cpu_baseline leg")

@@ -168,6 +168,10 @@ int tfft_scale(void *buf, int64_t count, int dtype_bytes, double s, void *stream
  * tuned default). Used by tools/tune.py; not needed by callers. */
 int tfft_tune_variants(int precision, int logn);
 int tfft_tune_select(int precision, int logn, int variant);
+/* Same for the multi-pass stage kernels of dim 2^logl; kind 0 = first stage,
+ * 1 = middle (3-stage), 2 = last. */
+int tfft_tune_pass_variants(int precision, int logl);
+int tfft_tune_pass_select(int precision, int logl, int kind, int variant);
 
 const char *tfft_last_error(void);
 int tfft_version(void);

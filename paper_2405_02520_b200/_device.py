@@ -50,7 +50,15 @@ def to_device(x, np_dtype, device=None):
 
 
 def to_host(t: torch.Tensor) -> np.ndarray:
-    return t.cpu().numpy()
+    """D2H into pinned memory from torch's caching host allocator (no page
+    faulting of fresh pageable memory per call); the numpy array keeps the
+    pinned block alive and returns it to the cache when dropped."""
+    if t.numel() * t.element_size() < (1 << 20):
+        return t.cpu().numpy()
+    h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+    h.copy_(t, non_blocking=True)
+    torch.cuda.current_stream(t.device).synchronize()
+    return h.numpy()
 
 
 def stream_ptr():

@@ -65,6 +65,8 @@ SIGNATURES = {
     "tfft_scale": (_INT, [_VP, _I64, _INT, _DBL, _VP]),
     "tfft_tune_variants": (_INT, [_INT, _INT]),
     "tfft_tune_select": (_INT, [_INT, _INT, _INT]),
+    "tfft_tune_pass_variants": (_INT, [_INT, _INT]),
+    "tfft_tune_pass_select": (_INT, [_INT, _INT, _INT, _INT]),
     "tfft_last_error": (ctypes.c_char_p, []),
     "tfft_version": (_INT, []),
 }

@@ -230,21 +230,47 @@ def _emit_single_index(parts):
     return "\n".join(lines) + "\n"
 
 
-# (E, radices, U) per log2 L for the multi-pass tile kernels (stage dims).
-PASS_TABLE = {
+# Multi-pass tile kernels (one launch per reference stage): candidates per
+# (precision, log2 L) as (E, radices, U, min CTAs/SM, prefetch), U = tile
+# width in transforms (row segment = U * sizeof(complex) bytes). Small L only
+# occur in user-built plans and keep one config. PASS_CHOICE picks a variant
+# per stage kind (first, middle, last) from tools/tune_pass.py.
+def _pc(*rows):
+    return [dict(e=r[0], radices=tuple(r[1]), u=r[2], minb=r[3], pf=r[4]) for r in rows]
+
+
+PASS_CANDIDATES = {
     "fp32": {
-        1: (2, (2,), 16), 2: (4, (4,), 16), 3: (8, (8,), 16), 4: (16, (16,), 16),
-        5: (8, (8, 4), 16), 6: (8, (8, 8), 16), 7: (16, (16, 8), 16),
-        8: (16, (16, 16), 16), 9: (16, (16, 16, 2), 16), 10: (16, (16, 16, 4), 8),
-        11: (16, (16, 16, 8), 4),
+        1: _pc((2, (2,), 16, 1, 0)), 2: _pc((4, (4,), 16, 1, 0)), 3: _pc((8, (8,), 16, 1, 0)),
+        4: _pc((16, (16,), 16, 1, 0)), 5: _pc((8, (8, 4), 16, 1, 0)), 6: _pc((8, (8, 8), 16, 1, 0)),
+        7: _pc((16, (16, 8), 16, 1, 0), (16, (16, 8), 16, 2, 1), (16, (16, 8), 8, 3, 1),
+               (8, (8, 8, 2), 16, 2, 1)),
+        8: _pc((16, (16, 16), 16, 1, 0), (16, (16, 16), 16, 2, 1), (16, (16, 16), 8, 3, 1),
+               (16, (16, 16), 8, 2, 0)),
+        9: _pc((16, (16, 16, 2), 16, 1, 0), (16, (16, 16, 2), 8, 2, 1), (16, (16, 16, 2), 4, 3, 1),
+               (16, (16, 16, 2), 8, 2, 0)),
+        10: _pc((16, (16, 16, 4), 8, 1, 0), (16, (16, 16, 4), 4, 2, 1), (16, (16, 16, 4), 4, 3, 0),
+                (32, (32, 32), 8, 1, 1), (16, (16, 16, 4), 8, 1, 1)),
+        11: _pc((16, (16, 16, 8), 4, 1, 0), (16, (16, 16, 8), 4, 2, 1), (16, (16, 16, 8), 2, 3, 1),
+                (32, (32, 16, 4), 4, 1, 1)),
     },
     "fp64": {
-        1: (2, (2,), 8), 2: (4, (4,), 8), 3: (8, (8,), 8), 4: (16, (16,), 8),
-        5: (8, (8, 4), 8), 6: (8, (8, 8), 8), 7: (16, (16, 8), 8),
-        8: (16, (16, 16), 8), 9: (8, (8, 8, 8), 8), 10: (8, (8, 8, 8, 2), 8),
-        11: (8, (8, 8, 8, 4), 4),
+        1: _pc((2, (2,), 8, 1, 0)), 2: _pc((4, (4,), 8, 1, 0)), 3: _pc((8, (8,), 8, 1, 0)),
+        4: _pc((16, (16,), 8, 1, 0)), 5: _pc((8, (8, 4), 8, 1, 0)), 6: _pc((8, (8, 8), 8, 1, 0)),
+        7: _pc((16, (16, 8), 8, 1, 0), (16, (16, 8), 8, 2, 1), (16, (16, 8), 4, 3, 1),
+               (8, (8, 8, 2), 8, 2, 1)),
+        8: _pc((16, (16, 16), 8, 1, 0), (16, (16, 16), 8, 2, 1), (16, (16, 16), 4, 2, 1),
+               (8, (8, 8, 4), 8, 2, 1)),
+        9: _pc((8, (8, 8, 8), 8, 1, 0), (8, (8, 8, 8), 4, 2, 1), (16, (16, 16, 2), 4, 2, 1),
+               (8, (8, 8, 8), 8, 1, 1)),
+        10: _pc((8, (8, 8, 8, 2), 8, 1, 0), (8, (8, 8, 8, 2), 4, 2, 1), (16, (16, 16, 4), 4, 1, 1),
+                (16, (16, 16, 4), 2, 2, 1)),
+        11: _pc((8, (8, 8, 8, 4), 4, 1, 0), (8, (8, 8, 8, 4), 2, 2, 1), (16, (16, 16, 8), 2, 1, 1),
+                (16, (16, 16, 8), 4, 1, 0)),
     },
 }
+# (first, middle, last) variant per log2 L; missing -> (0, 0, 0)
+PASS_CHOICE = {"fp32": {}, "fp64": {}}
 
 
 def tile_cost(l, e, radices, u, p, elem_bytes):
@@ -281,20 +307,23 @@ def tile_cost(l, e, radices, u, p, elem_bytes):
 
 def pass_configs():
     out = []
-    for prec, table in PASS_TABLE.items():
+    for prec, table in PASS_CANDIDATES.items():
         eb = ELEM_BYTES[prec]
-        for logl, (e, radices, u) in sorted(table.items()):
-            l = 1 << logl
-            assert math.prod(radices) == l and all(e % r == 0 for r in radices)
-            tps = l // e
-            u = max(u, 32 // tps)  # whole warps: the tile reductions use full-warp shuffles
-            threads = u * tps
-            assert threads <= 1024
-            best = min((tile_cost(l, e, radices, u, p, eb), p) for p in (1, 0, 2, 3, 4, 5, 8))
-            p = best[1]
-            smem = l * (u + p) * eb + 3 * (threads // 32 + 1) * (eb // 2)
-            out.append(dict(prec=prec, logl=logl, l=l, e=e, radices=radices, u=u, p=p,
-                            threads=threads, smem=smem))
+        for logl, cands in sorted(table.items()):
+            for vi, c in enumerate(cands):
+                l = 1 << logl
+                e, radices = c["e"], c["radices"]
+                assert math.prod(radices) == l and all(e % r == 0 for r in radices), (prec, logl, c)
+                tps = l // e
+                u = max(c["u"], 32 // tps)  # whole warps: the tile reductions use full-warp shuffles
+                threads = u * tps
+                assert threads <= 1024, (prec, logl, c)
+                best = min((tile_cost(l, e, radices, u, p, eb), p) for p in (1, 0, 2, 3, 4, 5, 8))
+                p = best[1]
+                nbuf = 2 if c["pf"] else 1
+                smem = nbuf * l * (u + p) * eb + 3 * (threads // 32 + 1) * (eb // 2)
+                out.append(dict(prec=prec, logl=logl, l=l, e=e, radices=radices, u=u, p=p,
+                                threads=threads, smem=smem, minb=c["minb"], pf=c["pf"], variant=vi))
     return out
 
 
@@ -308,21 +337,28 @@ def _emit_pass(prec, cfgs):
     entries = []
     for c in cfgs:
         rl = ", ".join(str(r) for r in c["radices"])
+
         def fn(kind, abft):
             return (f"(const void*)&fft_pass_kernel<{t}, {c['l']}, {c['e']}, {c['u']}, {c['p']}, "
-                    f"{kind}, {abft}, RList<{rl}>>")
+                    f"{kind}, {abft}, {c['minb']}, {c['pf']}, RList<{rl}>>")
         rows = [
             f"{{{fn(0, 0)}, {fn(0, 1)}, {fn(0, 1)}}}",
             f"{{{fn(1, 0)}, nullptr, nullptr}}",
             f"{{{fn(2, 0)}, {fn(2, 1)}, {fn(2, 2)}}}",
         ]
         entries.append(
-            f"    {{{c['logl']}, {c['e']}, {c['u']}, {c['p']}, {c['threads']}, {c['smem']}, "
-            f"{{{', '.join(rows)}}}}},  // radices {rl}")
+            f"    {{{c['logl']}, {c['variant']}, {c['e']}, {c['u']}, {c['p']}, {c['threads']}, "
+            f"{c['smem']}, {{{', '.join(rows)}}}}},  // radices {rl}, minb {c['minb']}, pf {c['pf']}")
     lines.append(f"const PassEntry kPass_{prec}[] = {{")
     lines += entries
     lines.append("};")
     lines.append(f"const int kPassCount_{prec} = {len(cfgs)};")
+    choice = PASS_CHOICE[prec]
+    lines.append(f"const int kPassChoice_{prec}[12][3] = {{")
+    for logl in range(12):
+        ch = choice.get(logl, (0, 0, 0))
+        lines.append(f"    {{{ch[0]}, {ch[1]}, {ch[2]}}},")
+    lines.append("};")
     lines.append("}  // namespace tfft")
     return "\n".join(lines) + "\n"
 

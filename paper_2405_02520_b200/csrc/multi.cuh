@@ -73,8 +73,25 @@ __device__ __forceinline__ void block_reduce(T (&v)[K], T* sh, int nwarps) {
     }
 }
 
-template <class T, int L, int E, int U, int P, int KIND, int ABFT, class Radices>
-__global__ void __launch_bounds__(U * (L / E))
+// element-granular async global->shared copy (SASS LDGSTS)
+template <int BYTES>
+__device__ __forceinline__ void cp_async(void* dst, const void* src) {
+    if constexpr (BYTES == 16)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(smem_u32(dst)), "l"(src), "n"(BYTES)
+                     : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// PF = 1: the CTA prefetches tile i+1 into the second half of a ping-pong
+// smem buffer with cp.async while tile i is transformed (the engine's
+// exchanges run in tile i's half), so HBM latency overlaps compute even at
+// one or two CTAs per SM.
+template <class T, int L, int E, int U, int P, int KIND, int ABFT, int MINB, int PF, class Radices>
+__global__ void __launch_bounds__(U * (L / E), MINB)
 fft_pass_kernel(const PassArgs<T> a) {
     constexpr int TPS = L / E;
     constexpr int THREADS = U * TPS;
@@ -82,7 +99,7 @@ fft_pass_kernel(const PassArgs<T> a) {
     using Eng = Engine<T, L, E, Radices>;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     C<T>* tile = reinterpret_cast<C<T>*>(smem_raw);
-    T* red = reinterpret_cast<T*>(tile + L * RS);
+    T* red = reinterpret_cast<T*>(tile + (PF ? 2 : 1) * L * RS);
 
     const int u = threadIdx.x % U;
     const int t = threadIdx.x / U;
@@ -95,9 +112,34 @@ fft_pass_kernel(const PassArgs<T> a) {
         __device__ __forceinline__ C<T> get(int i) const { return base[i * RS + u]; }
         __device__ __forceinline__ void sync() const { __syncthreads(); }
     };
-    const Mem mem{tile, u};
 
-    for (long long tix = blockIdx.x; tix < total; tix += gridDim.x) {
+    // async copy of tile `tx` into `buf` as [j][u] rows of stride RS
+    auto issue = [&](long long tx, C<T>* buf) {
+        const long long bb = tx / a.tiles_per_sig;
+        const long long v0 = (tx - bb * a.tiles_per_sig) * U;
+        const long long h0 = v0 / a.lo_count, l0 = v0 - h0 * a.lo_count;
+        const C<T>* sb = a.in + bb * a.n + h0 * a.in_hi + l0 * a.in_lo;
+        if constexpr (KIND == KIND_LAST) {  // U contiguous rows of L: j fastest
+            for (int f = threadIdx.x; f < U * L; f += THREADS) {
+                const int r = f / L, j = f % L;
+                cp_async<sizeof(C<T>)>(buf + j * RS + r, sb + (long long)r * a.in_lo + j);
+            }
+        } else {  // L strided rows of U contiguous elements: u fastest
+            for (int f = threadIdx.x; f < U * L; f += THREADS) {
+                const int r = f % U, j = f / U;
+                cp_async<sizeof(C<T>)>(buf + j * RS + r, sb + r * a.in_lo + (long long)j * a.in_j);
+            }
+        }
+    };
+    if constexpr (PF) {
+        if (blockIdx.x < total) issue(blockIdx.x, tile);
+        cp_async_commit();
+    }
+
+    unsigned it = 0;
+    for (long long tix = blockIdx.x; tix < total; tix += gridDim.x, ++it) {
+        C<T>* cur = (PF && (it & 1)) ? tile + L * RS : tile;
+        const Mem mem{cur, u};
         const long long b = tix / a.tiles_per_sig;
         const long long tsig = tix - b * a.tiles_per_sig;
         const long long u0 = tsig * U;               // first unit of the tile
@@ -112,7 +154,15 @@ fft_pass_kernel(const PassArgs<T> a) {
         const int fm = a.f_idx / TPS;
 
         C<T> v[E];
-        if constexpr (KIND == KIND_LAST) {
+        if constexpr (PF) {
+            if (tix + gridDim.x < total) issue(tix + gridDim.x, (it & 1) ? tile : tile + L * RS);
+            cp_async_commit();
+            cp_async_wait<1>();  // this tile's group has landed
+            __syncthreads();
+#pragma unroll
+            for (int m = 0; m < E; ++m) v[m] = cur[(t + m * TPS) * RS + u];
+            __syncthreads();
+        } else if constexpr (KIND == KIND_LAST) {
             // rows are contiguous: stage the U x L tile through smem with
             // j-fastest (fully coalesced) loads.
             const long long hi0 = u0 / a.lo_count, lo0 = u0 - hi0 * a.lo_count;
@@ -283,6 +333,7 @@ __global__ void __launch_bounds__(256) abft_finalize_kernel(const FinalArgs<T> a
 // ------------------------------------------------------------------ host
 struct PassEntry {
     int logl;
+    int variant;  // index into codegen.PASS_CANDIDATES[prec][logl]
     int e, u, p, threads, smem;
     const void* fn[3][3];  // [kind][abft]
 };
@@ -290,6 +341,11 @@ extern const PassEntry kPass_fp32[];
 extern const int kPassCount_fp32;
 extern const PassEntry kPass_fp64[];
 extern const int kPassCount_fp64;
+extern const int kPassChoice_fp32[12][3];  // tuned variant per (log2 L, kind)
+extern const int kPassChoice_fp64[12][3];
+// runtime override for tuning (-1 = tuned choice)
+int pass_tune_select(int prec, int logl, int kind, int variant);
+int pass_tune_variants(int prec, int logl);
 
 struct MultiPlan {
     int prec = 0;
@@ -297,7 +353,6 @@ struct MultiPlan {
     long long n = 0;
     long long d[3] = {0, 0, 0};
     int num_sms = 148;
-    const PassEntry* pe[3] = {nullptr, nullptr, nullptr};
     void* twL[3] = {nullptr, nullptr, nullptr};        // w_{d_k}^i tables
     void* ptw_lo[2] = {nullptr, nullptr};              // post twiddles per non-last stage
     void* ptw_hi[2] = {nullptr, nullptr};

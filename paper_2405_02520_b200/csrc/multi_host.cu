@@ -108,13 +108,26 @@ int upload_multires(int prec, long long L, void** dst) {
     return TFFT_OK;
 }
 
-const PassEntry* pass_entry(int prec, int logl) {
+int g_pass_override[2][12][3] = {};  // variant + 1; 0 = tuned choice
+
+const PassEntry* pass_variant(int prec, int logl, int variant) {
     const PassEntry* tab = prec == TFFT_FP32 ? kPass_fp32 : kPass_fp64;
     const int cnt = prec == TFFT_FP32 ? kPassCount_fp32 : kPassCount_fp64;
     for (int i = 0; i < cnt; ++i)
-        if (tab[i].logl == logl) return &tab[i];
+        if (tab[i].logl == logl && tab[i].variant == variant) return &tab[i];
     return nullptr;
 }
+
+// the entry stage kind `kind` of dim 2^logl launches
+const PassEntry* pass_entry(int prec, int logl, int kind) {
+    if (logl < 0 || logl >= 12) return nullptr;
+    const int ov = g_pass_override[prec][logl][kind];
+    const int v = ov > 0 ? ov - 1 : (prec == TFFT_FP32 ? kPassChoice_fp32 : kPassChoice_fp64)[logl][kind];
+    const PassEntry* e = pass_variant(prec, logl, v);
+    return e ? e : pass_variant(prec, logl, 0);
+}
+
+int kind_of(int k, int nst) { return k == 0 ? KIND_FIRST : (k == nst - 1 ? KIND_LAST : KIND_MID); }
 
 std::mutex occ_mu;
 std::map<const void*, int> occ;
@@ -168,9 +181,15 @@ int multi_launch_t(MultiPlan& mp, const MultiLaunch& m, cudaStream_t st) {
     }
     const bool abft = m.abft != ABFT_OFF;
     long long tiles[3];
+    const PassEntry* pe[3] = {nullptr, nullptr, nullptr};
     for (int k = 0; k < nst; ++k) {
+        pe[k] = pass_entry(mp.prec, lg(mp.d[k]), kind_of(k, nst));
+        if (!pe[k]) return merr(TFFT_EUNSUPPORTED, "no pass kernel for stage dim");
         const long long units = k == 0 ? R0 : (k == nst - 1 ? n / mp.d[k] : d0 * d2);
-        tiles[k] = units / mp.pe[k]->u;
+        const int kind = kind_of(k, nst);
+        const long long lo_count = kind == KIND_FIRST ? R0 : (kind == KIND_MID ? d2 : d0);
+        if (lo_count % pe[k]->u) return merr(TFFT_EUNSUPPORTED, "stage split too narrow for the tile width");
+        tiles[k] = units / pe[k]->u;
     }
     T* part_in = nullptr;
     T* part_out = nullptr;
@@ -263,7 +282,7 @@ int multi_launch_t(MultiPlan& mp, const MultiLaunch& m, cudaStream_t st) {
                 }
             }
         }
-        int rc = launch_pass<T>(mp, mp.pe[k], kind, abft_v, a, mp.num_sms, st);
+        int rc = launch_pass<T>(mp, pe[k], kind, abft_v, a, mp.num_sms, st);
         if (rc) return rc;
     }
     if (abft) {
@@ -294,6 +313,20 @@ int multi_launch_t(MultiPlan& mp, const MultiLaunch& m, cudaStream_t st) {
 
 const char* multi_last_error() { return m_err.c_str(); }
 
+int pass_tune_variants(int prec, int logl) {
+    int n = 0;
+    while (pass_variant(prec, logl, n)) ++n;
+    return n;
+}
+
+int pass_tune_select(int prec, int logl, int kind, int variant) {
+    if ((prec != TFFT_FP32 && prec != TFFT_FP64) || logl < 1 || logl >= 12 || kind < 0 || kind > 2)
+        return merr(TFFT_EINVAL, "bad pass selector");
+    if (variant >= 0 && !pass_variant(prec, logl, variant)) return merr(TFFT_EINVAL, "no such pass variant");
+    g_pass_override[prec][logl][kind] = variant < 0 ? 0 : variant + 1;
+    return TFFT_OK;
+}
+
 int multi_plan_init(MultiPlan& mp, long long n, int prec, int nst, const int64_t* dims, int num_sms) {
     mp.prec = prec;
     mp.nst = nst;
@@ -303,11 +336,11 @@ int multi_plan_init(MultiPlan& mp, long long n, int prec, int nst, const int64_t
     for (int k = 0; k < nst; ++k) mp.d[k] = dims[k];
     const long long R0 = n / mp.d[0];
     for (int k = 0; k < nst; ++k) {
-        mp.pe[k] = pass_entry(prec, lg(mp.d[k]));
-        if (!mp.pe[k]) return merr(TFFT_EUNSUPPORTED, "no pass kernel for stage dim");
-        const int kind = k == 0 ? KIND_FIRST : (k == nst - 1 ? KIND_LAST : KIND_MID);
+        const int kind = kind_of(k, nst);
+        const PassEntry* pe = pass_entry(prec, lg(mp.d[k]), kind);
+        if (!pe) return merr(TFFT_EUNSUPPORTED, "no pass kernel for stage dim");
         const long long lo_count = kind == KIND_FIRST ? R0 : (kind == KIND_MID ? mp.d[2] : mp.d[0]);
-        if (lo_count % mp.pe[k]->u) return merr(TFFT_EUNSUPPORTED, "stage split too narrow for the tile width");
+        if (lo_count % pe->u) return merr(TFFT_EUNSUPPORTED, "stage split too narrow for the tile width");
         int rc = upload_multires(prec, mp.d[k], &mp.twL[k]);
         if (rc) return rc;
         if (kind != KIND_LAST) {

@@ -323,6 +323,17 @@ int tfft_tune_variants(int precision, int logn) {
     return single_index().count[precision][logn];
 }
 
+int tfft_tune_pass_variants(int precision, int logl) {
+    if ((precision != TFFT_FP32 && precision != TFFT_FP64) || logl < 1 || logl >= 12) return 0;
+    return pass_tune_variants(precision, logl);
+}
+
+int tfft_tune_pass_select(int precision, int logl, int kind, int variant) {
+    int rc = pass_tune_select(precision, logl, kind, variant);
+    if (rc) return fail(rc, multi_last_error());
+    return TFFT_OK;
+}
+
 int tfft_tune_select(int precision, int logn, int variant) {
     if ((precision != TFFT_FP32 && precision != TFFT_FP64) || logn < 1 || logn > 13)
         return fail(TFFT_EINVAL, "no single-kernel size");
