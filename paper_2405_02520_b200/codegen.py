@@ -269,8 +269,12 @@ PASS_CANDIDATES = {
                 (16, (16, 16, 8), 4, 1, 0)),
     },
 }
-# (first, middle, last) variant per log2 L; missing -> (0, 0, 0)
-PASS_CHOICE = {"fp32": {}, "fp64": {}}
+# (first, middle, last) variant per log2 L; missing -> (0, 0, 0).
+# Source: tools/tune_pass.py on a B200, ABFT on, 1 GiB (profiles/tune_pass_r01.json).
+PASS_CHOICE = {
+    "fp32": {7: (0, 1, 1), 8: (1, 1, 1), 9: (0, 0, 2), 10: (0, 0, 2), 11: (0, 0, 3)},
+    "fp64": {7: (0, 0, 2), 8: (0, 1, 2), 9: (1, 0, 1), 10: (0, 0, 0), 11: (0, 0, 3)},
+}
 
 
 def tile_cost(l, e, radices, u, p, elem_bytes):
