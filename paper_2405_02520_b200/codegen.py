@@ -29,16 +29,18 @@ def _cands(*rows):
 
 SINGLE_CANDIDATES = {
     "fp32": {
-        1: _cands((2, (2,), 256, 1, 1), (2, (2,), 256, 1, 0)),
-        2: _cands((4, (4,), 256, 1, 1), (4, (4,), 256, 1, 0)),
+        1: _cands((2, (2,), 256, 1, 1), (2, (2,), 256, 1, 0), (2, (2,), 256, 1, 3)),
+        2: _cands((4, (4,), 256, 1, 1), (4, (4,), 256, 1, 0), (4, (4,), 256, 1, 3)),
         3: _cands((8, (8,), 256, 1, 1), (8, (8,), 256, 1, 0), (4, (4, 2), 256, 1, 1),
-                  (8, (8,), 128, 1, 1)),
+                  (8, (8,), 128, 1, 1), (8, (8,), 128, 1, 3), (8, (8,), 256, 1, 3),
+                  (4, (4, 2), 256, 1, 3)),
         4: _cands((16, (16,), 256, 1, 1), (16, (16,), 256, 1, 0), (8, (8, 2), 256, 1, 1),
-                  (4, (4, 4), 256, 1, 1), (16, (16,), 128, 1, 1)),
+                  (4, (4, 4), 256, 1, 1), (16, (16,), 128, 1, 1), (16, (16,), 128, 1, 3),
+                  (8, (8, 2), 256, 1, 3)),
         5: _cands((8, (8, 4), 256, 1, 1), (8, (8, 4), 256, 1, 0), (16, (16, 2), 256, 1, 1),
-                  (32, (32,), 256, 1, 1)),
+                  (32, (32,), 256, 1, 1), (8, (8, 4), 256, 1, 3), (8, (8, 4), 256, 1, 2)),
         6: _cands((8, (8, 8), 256, 1, 1), (8, (8, 8), 256, 1, 0), (16, (16, 4), 256, 1, 1),
-                  (16, (16, 4), 256, 1, 0)),
+                  (16, (16, 4), 256, 1, 0), (8, (8, 8), 256, 1, 3), (8, (8, 8), 256, 1, 2)),
         7: _cands((16, (16, 8), 256, 1, 0), (16, (16, 8), 256, 1, 1), (8, (8, 8, 2), 256, 1, 0),
                   (16, (16, 8), 256, 3, 0), (16, (16, 8), 256, 1, 2)),
         8: _cands((16, (16, 16), 256, 1, 0), (16, (16, 16), 256, 3, 0), (8, (8, 8, 4), 256, 1, 0),
@@ -61,12 +63,16 @@ SINGLE_CANDIDATES = {
                    (16, (16, 16, 16, 2), 512, 2, 2), (16, (16, 16, 16, 2), 512, 1, 2)),
     },
     "fp64": {
-        1: _cands((2, (2,), 256, 1, 1), (2, (2,), 256, 1, 0)),
-        2: _cands((4, (4,), 256, 1, 1), (4, (4,), 256, 1, 0)),
-        3: _cands((8, (8,), 256, 1, 1), (8, (8,), 256, 1, 0), (4, (4, 2), 256, 1, 1)),
-        4: _cands((16, (16,), 256, 1, 1), (8, (8, 2), 256, 1, 1), (4, (4, 4), 256, 1, 1)),
-        5: _cands((8, (8, 4), 256, 1, 1), (8, (8, 4), 256, 1, 0), (16, (16, 2), 256, 1, 1)),
-        6: _cands((8, (8, 8), 256, 1, 1), (8, (8, 8), 256, 1, 0), (16, (16, 4), 256, 1, 0)),
+        1: _cands((2, (2,), 256, 1, 1), (2, (2,), 256, 1, 0), (2, (2,), 256, 1, 3)),
+        2: _cands((4, (4,), 256, 1, 1), (4, (4,), 256, 1, 0), (4, (4,), 256, 1, 3)),
+        3: _cands((8, (8,), 256, 1, 1), (8, (8,), 256, 1, 0), (4, (4, 2), 256, 1, 1),
+                  (8, (8,), 128, 1, 3), (8, (8,), 256, 1, 3)),
+        4: _cands((16, (16,), 256, 1, 1), (8, (8, 2), 256, 1, 1), (4, (4, 4), 256, 1, 1),
+                  (8, (8, 2), 256, 1, 3), (16, (16,), 128, 1, 3)),
+        5: _cands((8, (8, 4), 256, 1, 1), (8, (8, 4), 256, 1, 0), (16, (16, 2), 256, 1, 1),
+                  (8, (8, 4), 256, 1, 3), (8, (8, 4), 256, 1, 2)),
+        6: _cands((8, (8, 8), 256, 1, 1), (8, (8, 8), 256, 1, 0), (16, (16, 4), 256, 1, 0),
+                  (8, (8, 8), 256, 1, 3), (8, (8, 8), 256, 1, 2)),
         7: _cands((16, (16, 8), 256, 1, 0), (8, (8, 8, 2), 256, 1, 0), (16, (16, 8), 256, 1, 1),
                   (16, (16, 8), 256, 1, 2)),
         8: _cands((16, (16, 16), 256, 1, 0), (8, (8, 8, 4), 256, 1, 0), (16, (16, 16), 256, 2, 0),
@@ -172,8 +178,8 @@ def single_configs(all_candidates=True):
                 ps, _ = choose_padding(n, e, radices, prec)
                 s = threads // tps
                 ex = (n + (n >> ps) + 1 if ps else n) if len(radices) > 1 else 0
-                st = n + 1 if c["stage"] == 1 else 0
-                ib = s * n if c["stage"] == 2 else 0  # TMA prefetch buffer
+                st = n + 1 if c["stage"] in (1, 3) else 0
+                ib = s * n if c["stage"] in (2, 3) else 0  # TMA prefetch buffer
                 smem = ((ib + s * max(ex, st)) * ELEM_BYTES[prec]
                         + 5 * (threads // 32 + 1) * (ELEM_BYTES[prec] // 2))
                 out.append(dict(prec=prec, logn=logn, n=n, e=e, radices=radices, threads=threads,

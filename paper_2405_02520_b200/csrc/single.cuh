@@ -145,8 +145,10 @@ fft_single_kernel(const SingleArgs<T> a) {
     // STAGE: 0 direct coalesced loads, 1 CTA-staged vector I/O (short
     // signals), 2 TMA bulk prefetch of the next tile into smem (cp.async.bulk
     // + mbarrier) while the current tile computes.
-    constexpr bool STG = STAGE == 1;
-    constexpr bool PF = STAGE == 2;
+    // 3: both — TMA prefetch of the next contiguous chunk, then an on-chip
+    // reshuffle into the padded staging slices (short signals).
+    constexpr bool STG = STAGE == 1 || STAGE == 3;
+    constexpr bool PF = STAGE == 2 || STAGE == 3;
     constexpr bool MULTIPASS = RCount<Radices>::v > 1;
     constexpr int SL = SliceLen<N, PS, MULTIPASS, STG>::v;
     constexpr int NW = THREADS / 32 > 0 ? THREADS / 32 : 1;
@@ -185,7 +187,27 @@ fft_single_kernel(const SingleArgs<T> a) {
         const long long valid = (a.batch - tile * S) * N;  // elements of this CTA chunk in range
 
         C<T> v[E];
-        if constexpr (PF) {
+        if constexpr (PF && STG) {
+            mbar_wait(&in_bar, iter & 1);
+            // contiguous chunk -> padded slices (16-byte reads, 8-byte writes)
+            for (int e = threadIdx.x * (16 / (int)sizeof(C<T>)); e < S * N; e += THREADS * (16 / (int)sizeof(C<T>))) {
+                if constexpr (sizeof(T) == 4) {
+                    const float4 q = reinterpret_cast<const float4*>(ib)[e / 2];
+                    sm_all[(e / N) * SL + e % N] = make_float2(q.x, q.y);
+                    sm_all[(e / N) * SL + e % N + 1] = make_float2(q.z, q.w);
+                } else {
+                    sm_all[(e / N) * SL + e % N] = ib[e];
+                }
+            }
+            __syncthreads();  // chunk consumed: refill the buffer
+            if (threadIdx.x == 0 && tile + gridDim.x < tiles) {
+                fence_proxy_async();
+                prefetch(tile + gridDim.x);
+            }
+#pragma unroll
+            for (int m = 0; m < E; ++m) v[m] = live ? sm[t + m * TPS] : mk<T>(T(0), T(0));
+            __syncthreads();
+        } else if constexpr (PF) {
             mbar_wait(&in_bar, iter & 1);
 #pragma unroll
             for (int m = 0; m < E; ++m) v[m] = live ? ib[sl * N + t + m * TPS] : mk<T>(T(0), T(0));
