@@ -91,8 +91,8 @@ SINGLE_CANDIDATES = {
 # tuned winners (index into SINGLE_CANDIDATES[prec][logn]); missing -> 0.
 # Source: tools/tune.py on a B200, ABFT on, 1 GiB batches (profiles/tune_r01.json).
 SINGLE_CHOICE = {
-    "fp32": {1: 1, 2: 1, 3: 3, 4: 4, 5: 1, 6: 1, 7: 0, 8: 4, 9: 0, 10: 1, 11: 5, 12: 5, 13: 5},
-    "fp64": {1: 1, 2: 1, 3: 0, 4: 1, 5: 1, 6: 1, 7: 3, 8: 2, 9: 3, 10: 2, 11: 1, 12: 1, 13: 0},
+    "fp32": {1: 1, 2: 1, 3: 4, 4: 5, 5: 1, 6: 1, 7: 0, 8: 4, 9: 0, 10: 1, 11: 5, 12: 5, 13: 5},
+    "fp64": {1: 1, 2: 1, 3: 3, 4: 3, 5: 1, 6: 1, 7: 3, 8: 2, 9: 3, 10: 2, 11: 1, 12: 1, 13: 0},
 }
 ELEM_BYTES = {"fp32": 8, "fp64": 16}
 CTYPE = {"fp32": "float", "fp64": "double"}
@@ -250,29 +250,30 @@ PASS_CANDIDATES = {
         1: _pc((2, (2,), 16, 1, 0)), 2: _pc((4, (4,), 16, 1, 0)), 3: _pc((8, (8,), 16, 1, 0)),
         4: _pc((16, (16,), 16, 1, 0)), 5: _pc((8, (8, 4), 16, 1, 0)), 6: _pc((8, (8, 8), 16, 1, 0)),
         7: _pc((16, (16, 8), 16, 1, 0), (16, (16, 8), 16, 2, 1), (16, (16, 8), 8, 3, 1),
-               (8, (8, 8, 2), 16, 2, 1)),
+               (8, (8, 8, 2), 16, 2, 1), (16, (16, 8), 16, 2, 2), (16, (16, 8), 8, 3, 2)),
         8: _pc((16, (16, 16), 16, 1, 0), (16, (16, 16), 16, 2, 1), (16, (16, 16), 8, 3, 1),
-               (16, (16, 16), 8, 2, 0)),
+               (16, (16, 16), 8, 2, 0), (16, (16, 16), 16, 2, 2), (16, (16, 16), 8, 3, 2)),
         9: _pc((16, (16, 16, 2), 16, 1, 0), (16, (16, 16, 2), 8, 2, 1), (16, (16, 16, 2), 4, 3, 1),
-               (16, (16, 16, 2), 8, 2, 0)),
+               (16, (16, 16, 2), 8, 2, 0), (16, (16, 16, 2), 8, 2, 2), (16, (16, 16, 2), 16, 1, 2)),
         10: _pc((16, (16, 16, 4), 8, 1, 0), (16, (16, 16, 4), 4, 2, 1), (16, (16, 16, 4), 4, 3, 0),
-                (32, (32, 32), 8, 1, 1), (16, (16, 16, 4), 8, 1, 1)),
+                (32, (32, 32), 8, 1, 1), (16, (16, 16, 4), 8, 1, 1), (16, (16, 16, 4), 8, 1, 2),
+                (16, (16, 16, 4), 4, 2, 2)),
         11: _pc((16, (16, 16, 8), 4, 1, 0), (16, (16, 16, 8), 4, 2, 1), (16, (16, 16, 8), 2, 3, 1),
-                (32, (32, 16, 4), 4, 1, 1)),
+                (32, (32, 16, 4), 4, 1, 1), (16, (16, 16, 8), 4, 1, 2), (16, (16, 16, 8), 2, 2, 2)),
     },
     "fp64": {
         1: _pc((2, (2,), 8, 1, 0)), 2: _pc((4, (4,), 8, 1, 0)), 3: _pc((8, (8,), 8, 1, 0)),
         4: _pc((16, (16,), 8, 1, 0)), 5: _pc((8, (8, 4), 8, 1, 0)), 6: _pc((8, (8, 8), 8, 1, 0)),
         7: _pc((16, (16, 8), 8, 1, 0), (16, (16, 8), 8, 2, 1), (16, (16, 8), 4, 3, 1),
-               (8, (8, 8, 2), 8, 2, 1)),
+               (8, (8, 8, 2), 8, 2, 1), (16, (16, 8), 8, 2, 2), (16, (16, 8), 4, 3, 2)),
         8: _pc((16, (16, 16), 8, 1, 0), (16, (16, 16), 8, 2, 1), (16, (16, 16), 4, 2, 1),
-               (8, (8, 8, 4), 8, 2, 1)),
+               (8, (8, 8, 4), 8, 2, 1), (16, (16, 16), 8, 2, 2), (8, (8, 8, 4), 8, 2, 2)),
         9: _pc((8, (8, 8, 8), 8, 1, 0), (8, (8, 8, 8), 4, 2, 1), (16, (16, 16, 2), 4, 2, 1),
-               (8, (8, 8, 8), 8, 1, 1)),
+               (8, (8, 8, 8), 8, 1, 1), (8, (8, 8, 8), 8, 1, 2), (8, (8, 8, 8), 4, 2, 2)),
         10: _pc((8, (8, 8, 8, 2), 8, 1, 0), (8, (8, 8, 8, 2), 4, 2, 1), (16, (16, 16, 4), 4, 1, 1),
-                (16, (16, 16, 4), 2, 2, 1)),
+                (16, (16, 16, 4), 2, 2, 1), (8, (8, 8, 8, 2), 4, 1, 2), (8, (8, 8, 8, 2), 2, 2, 2)),
         11: _pc((8, (8, 8, 8, 4), 4, 1, 0), (8, (8, 8, 8, 4), 2, 2, 1), (16, (16, 16, 8), 2, 1, 1),
-                (16, (16, 16, 8), 4, 1, 0)),
+                (16, (16, 16, 8), 4, 1, 0), (8, (8, 8, 8, 4), 2, 1, 2), (8, (8, 8, 8, 4), 2, 2, 2)),
     },
 }
 # (first, middle, last) variant per log2 L; missing -> (0, 0, 0).
@@ -331,7 +332,11 @@ def pass_configs():
                 best = min((tile_cost(l, e, radices, u, p, eb), p) for p in (1, 0, 2, 3, 4, 5, 8))
                 p = best[1]
                 nbuf = 2 if c["pf"] else 1
-                smem = nbuf * l * (u + p) * eb + 3 * (threads // 32 + 1) * (eb // 2)
+                bufe = l * (u + p)
+                if c["pf"] == 2:  # bulk staging: last-kind rows at a padded stride
+                    su = l + 2 if prec == "fp32" else l + 1
+                    bufe = max(bufe, u * su)
+                smem = nbuf * bufe * eb + 3 * (threads // 32 + 1) * (eb // 2)
                 out.append(dict(prec=prec, logl=logl, l=l, e=e, radices=radices, u=u, p=p,
                                 threads=threads, smem=smem, minb=c["minb"], pf=c["pf"], variant=vi))
     return out

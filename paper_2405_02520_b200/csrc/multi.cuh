@@ -96,10 +96,18 @@ fft_pass_kernel(const PassArgs<T> a) {
     constexpr int TPS = L / E;
     constexpr int THREADS = U * TPS;
     constexpr int RS = U + P;  // smem row stride (elements) of the [L][U] tile
+    // PF = 2: per-row TMA bulk copies (cp.async.bulk, one instruction per row
+    // segment, no per-element issue work) into a dense staging layout, two
+    // buffers on two mbarriers. Rows of the last kind land at a padded stride.
+    constexpr bool BULK = PF == 2;
+    constexpr int SU = sizeof(T) == 4 ? L + 2 : L + 1;  // 16-byte aligned padded row
+    constexpr int BUFE = BULK ? (L * RS > U * SU ? L * RS : U * SU) : L * RS;
+    constexpr int ISSUERS = KIND == KIND_LAST ? U : (L < THREADS ? L : THREADS);
     using Eng = Engine<T, L, E, Radices>;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     C<T>* tile = reinterpret_cast<C<T>*>(smem_raw);
-    T* red = reinterpret_cast<T*>(tile + (PF ? 2 : 1) * L * RS);
+    T* red = reinterpret_cast<T*>(tile + (PF ? 2 : 1) * BUFE);
+    __shared__ unsigned long long bbar[2];
 
     const int u = threadIdx.x % U;
     const int t = threadIdx.x / U;
@@ -131,14 +139,43 @@ fft_pass_kernel(const PassArgs<T> a) {
             }
         }
     };
-    if constexpr (PF) {
+    // bulk variant: the ISSUERS threads each arrive with their byte count
+    auto issue_bulk = [&](long long tx, C<T>* buf, unsigned long long* bar) {
+        if (threadIdx.x >= ISSUERS) return;
+        const long long bb = tx / a.tiles_per_sig;
+        const long long v0 = (tx - bb * a.tiles_per_sig) * U;
+        const long long h0 = v0 / a.lo_count, l0 = v0 - h0 * a.lo_count;
+        const C<T>* sb = a.in + bb * a.n + h0 * a.in_hi + l0 * a.in_lo;
+        fence_proxy_async();
+        if constexpr (KIND == KIND_LAST) {  // row u: L contiguous elements
+            const unsigned bytes = L * sizeof(C<T>);
+            mbar_expect_tx(bar, bytes);
+            bulk_g2s(buf + threadIdx.x * SU, sb + (long long)threadIdx.x * a.in_lo, bytes, bar);
+        } else {  // rows j: U contiguous elements each, dense [j][U]
+            constexpr int RPI = L / ISSUERS;
+            mbar_expect_tx(bar, RPI * U * sizeof(C<T>));
+#pragma unroll
+            for (int k = 0; k < RPI; ++k) {
+                const int j = threadIdx.x + k * ISSUERS;
+                bulk_g2s(buf + j * U, sb + (long long)j * a.in_j, U * sizeof(C<T>), bar);
+            }
+        }
+    };
+    if constexpr (BULK) {
+        if (threadIdx.x == 0) {
+            mbar_init(&bbar[0], ISSUERS);
+            mbar_init(&bbar[1], ISSUERS);
+        }
+        __syncthreads();
+        if (blockIdx.x < total) issue_bulk(blockIdx.x, tile, &bbar[0]);
+    } else if constexpr (PF) {
         if (blockIdx.x < total) issue(blockIdx.x, tile);
         cp_async_commit();
     }
 
     unsigned it = 0;
     for (long long tix = blockIdx.x; tix < total; tix += gridDim.x, ++it) {
-        C<T>* cur = (PF && (it & 1)) ? tile + L * RS : tile;
+        C<T>* cur = (PF && (it & 1)) ? tile + BUFE : tile;
         const Mem mem{cur, u};
         const long long b = tix / a.tiles_per_sig;
         const long long tsig = tix - b * a.tiles_per_sig;
@@ -154,8 +191,20 @@ fft_pass_kernel(const PassArgs<T> a) {
         const int fm = a.f_idx / TPS;
 
         C<T> v[E];
-        if constexpr (PF) {
-            if (tix + gridDim.x < total) issue(tix + gridDim.x, (it & 1) ? tile : tile + L * RS);
+        if constexpr (BULK) {
+            if (tix + gridDim.x < total)
+                issue_bulk(tix + gridDim.x, (it & 1) ? tile : tile + BUFE, &bbar[(it + 1) & 1]);
+            mbar_wait(&bbar[it & 1], (it >> 1) & 1);
+            if constexpr (KIND == KIND_LAST) {
+#pragma unroll
+                for (int m = 0; m < E; ++m) v[m] = cur[u * SU + t + m * TPS];
+            } else {
+#pragma unroll
+                for (int m = 0; m < E; ++m) v[m] = cur[(t + m * TPS) * U + u];
+            }
+            __syncthreads();
+        } else if constexpr (PF) {
+            if (tix + gridDim.x < total) issue(tix + gridDim.x, (it & 1) ? tile : tile + BUFE);
             cp_async_commit();
             cp_async_wait<1>();  // this tile's group has landed
             __syncthreads();
