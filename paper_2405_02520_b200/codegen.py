@@ -250,37 +250,46 @@ PASS_CANDIDATES = {
         1: _pc((2, (2,), 16, 1, 0)), 2: _pc((4, (4,), 16, 1, 0)), 3: _pc((8, (8,), 16, 1, 0)),
         4: _pc((16, (16,), 16, 1, 0)), 5: _pc((8, (8, 4), 16, 1, 0)), 6: _pc((8, (8, 8), 16, 1, 0)),
         7: _pc((16, (16, 8), 16, 1, 0), (16, (16, 8), 16, 2, 1), (16, (16, 8), 8, 3, 1),
-               (8, (8, 8, 2), 16, 2, 1), (16, (16, 8), 16, 2, 2), (16, (16, 8), 8, 3, 2)),
+               (8, (8, 8, 2), 16, 2, 1), (16, (16, 8), 16, 2, 2), (16, (16, 8), 8, 3, 2),
+               (16, (16, 8), 16, 2, 3), (16, (16, 8), 8, 3, 3)),
         8: _pc((16, (16, 16), 16, 1, 0), (16, (16, 16), 16, 2, 1), (16, (16, 16), 8, 3, 1),
-               (16, (16, 16), 8, 2, 0), (16, (16, 16), 16, 2, 2), (16, (16, 16), 8, 3, 2)),
+               (16, (16, 16), 8, 2, 0), (16, (16, 16), 16, 2, 2), (16, (16, 16), 8, 3, 2),
+               (16, (16, 16), 16, 2, 3), (16, (16, 16), 8, 3, 3)),
         9: _pc((16, (16, 16, 2), 16, 1, 0), (16, (16, 16, 2), 8, 2, 1), (16, (16, 16, 2), 4, 3, 1),
-               (16, (16, 16, 2), 8, 2, 0), (16, (16, 16, 2), 8, 2, 2), (16, (16, 16, 2), 16, 1, 2)),
+               (16, (16, 16, 2), 8, 2, 0), (16, (16, 16, 2), 8, 2, 2), (16, (16, 16, 2), 16, 1, 2),
+               (16, (16, 16, 2), 16, 1, 3), (16, (16, 16, 2), 8, 2, 3)),
         10: _pc((16, (16, 16, 4), 8, 1, 0), (16, (16, 16, 4), 4, 2, 1), (16, (16, 16, 4), 4, 3, 0),
                 (32, (32, 32), 8, 1, 1), (16, (16, 16, 4), 8, 1, 1), (16, (16, 16, 4), 8, 1, 2),
-                (16, (16, 16, 4), 4, 2, 2)),
+                (16, (16, 16, 4), 4, 2, 2), (16, (16, 16, 4), 8, 1, 3), (16, (16, 16, 4), 4, 2, 3)),
         11: _pc((16, (16, 16, 8), 4, 1, 0), (16, (16, 16, 8), 4, 2, 1), (16, (16, 16, 8), 2, 3, 1),
-                (32, (32, 16, 4), 4, 1, 1), (16, (16, 16, 8), 4, 1, 2), (16, (16, 16, 8), 2, 2, 2)),
+                (32, (32, 16, 4), 4, 1, 1), (16, (16, 16, 8), 4, 1, 2), (16, (16, 16, 8), 2, 2, 2),
+                (16, (16, 16, 8), 4, 1, 3), (16, (16, 16, 8), 2, 2, 3)),
     },
     "fp64": {
         1: _pc((2, (2,), 8, 1, 0)), 2: _pc((4, (4,), 8, 1, 0)), 3: _pc((8, (8,), 8, 1, 0)),
         4: _pc((16, (16,), 8, 1, 0)), 5: _pc((8, (8, 4), 8, 1, 0)), 6: _pc((8, (8, 8), 8, 1, 0)),
         7: _pc((16, (16, 8), 8, 1, 0), (16, (16, 8), 8, 2, 1), (16, (16, 8), 4, 3, 1),
-               (8, (8, 8, 2), 8, 2, 1), (16, (16, 8), 8, 2, 2), (16, (16, 8), 4, 3, 2)),
+               (8, (8, 8, 2), 8, 2, 1), (16, (16, 8), 8, 2, 2), (16, (16, 8), 4, 3, 2),
+               (16, (16, 8), 8, 2, 3), (16, (16, 8), 4, 3, 3)),
         8: _pc((16, (16, 16), 8, 1, 0), (16, (16, 16), 8, 2, 1), (16, (16, 16), 4, 2, 1),
-               (8, (8, 8, 4), 8, 2, 1), (16, (16, 16), 8, 2, 2), (8, (8, 8, 4), 8, 2, 2)),
+               (8, (8, 8, 4), 8, 2, 1), (16, (16, 16), 8, 2, 2), (8, (8, 8, 4), 8, 2, 2),
+               (16, (16, 16), 8, 2, 3), (8, (8, 8, 4), 8, 2, 3)),
         9: _pc((8, (8, 8, 8), 8, 1, 0), (8, (8, 8, 8), 4, 2, 1), (16, (16, 16, 2), 4, 2, 1),
-               (8, (8, 8, 8), 8, 1, 1), (8, (8, 8, 8), 8, 1, 2), (8, (8, 8, 8), 4, 2, 2)),
+               (8, (8, 8, 8), 8, 1, 1), (8, (8, 8, 8), 8, 1, 2), (8, (8, 8, 8), 4, 2, 2),
+               (8, (8, 8, 8), 8, 1, 3), (8, (8, 8, 8), 4, 2, 3)),
         10: _pc((8, (8, 8, 8, 2), 8, 1, 0), (8, (8, 8, 8, 2), 4, 2, 1), (16, (16, 16, 4), 4, 1, 1),
-                (16, (16, 16, 4), 2, 2, 1), (8, (8, 8, 8, 2), 4, 1, 2), (8, (8, 8, 8, 2), 2, 2, 2)),
+                (16, (16, 16, 4), 2, 2, 1), (8, (8, 8, 8, 2), 4, 1, 2), (8, (8, 8, 8, 2), 2, 2, 2),
+                (8, (8, 8, 8, 2), 4, 1, 3), (8, (8, 8, 8, 2), 2, 2, 3)),
         11: _pc((8, (8, 8, 8, 4), 4, 1, 0), (8, (8, 8, 8, 4), 2, 2, 1), (16, (16, 16, 8), 2, 1, 1),
-                (16, (16, 16, 8), 4, 1, 0), (8, (8, 8, 8, 4), 2, 1, 2), (8, (8, 8, 8, 4), 2, 2, 2)),
+                (16, (16, 16, 8), 4, 1, 0), (8, (8, 8, 8, 4), 2, 1, 2), (8, (8, 8, 8, 4), 2, 2, 2),
+                (8, (8, 8, 8, 4), 2, 1, 3), (8, (8, 8, 8, 4), 2, 2, 3)),
     },
 }
 # (first, middle, last) variant per log2 L; missing -> (0, 0, 0).
 # Source: tools/tune_pass.py on a B200, ABFT on, 1 GiB (profiles/tune_pass_r01.json).
 PASS_CHOICE = {
-    "fp32": {7: (0, 1, 1), 8: (1, 1, 1), 9: (0, 0, 2), 10: (0, 0, 2), 11: (0, 0, 3)},
-    "fp64": {7: (0, 0, 2), 8: (0, 1, 2), 9: (1, 0, 1), 10: (0, 0, 0), 11: (0, 0, 3)},
+    "fp32": {7: (0, 1, 5), 8: (4, 1, 5), 9: (0, 0, 4), 10: (0, 0, 6), 11: (0, 0, 4)},
+    "fp64": {7: (0, 0, 4), 8: (5, 1, 4), 9: (1, 0, 5), 10: (0, 0, 4), 11: (0, 0, 3)},
 }
 
 
@@ -333,7 +342,7 @@ def pass_configs():
                 p = best[1]
                 nbuf = 2 if c["pf"] else 1
                 bufe = l * (u + p)
-                if c["pf"] == 2:  # bulk staging: last-kind rows at a padded stride
+                if c["pf"] in (2, 3):  # bulk staging: last-kind rows at a padded stride
                     su = l + 2 if prec == "fp32" else l + 1
                     bufe = max(bufe, u * su)
                 smem = nbuf * bufe * eb + 3 * (threads // 32 + 1) * (eb // 2)
@@ -362,7 +371,7 @@ def _emit_pass(prec, cfgs):
             f"{{{fn(2, 0)}, {fn(2, 1)}, {fn(2, 2)}}}",
         ]
         entries.append(
-            f"    {{{c['logl']}, {c['variant']}, {c['e']}, {c['u']}, {c['p']}, {c['threads']}, "
+            f"    {{{c['logl']}, {c['variant']}, {c['pf']}, {c['e']}, {c['u']}, {c['p']}, {c['threads']}, "
             f"{c['smem']}, {{{', '.join(rows)}}}}},  // radices {rl}, minb {c['minb']}, pf {c['pf']}")
     lines.append(f"const PassEntry kPass_{prec}[] = {{")
     lines += entries

@@ -22,6 +22,8 @@
 // A finalize kernel reduces the tile partials per signal in a fixed order and
 // takes the detection decision (reference abft/pipeline.py:104-135).
 #pragma once
+#include <cuda.h>  // CUtensorMap (TMA descriptor; encoded on the host per launch)
+
 #include "single.cuh"
 
 namespace tfft {
@@ -29,7 +31,8 @@ namespace tfft {
 enum { KIND_FIRST = 0, KIND_MID = 1, KIND_LAST = 2 };
 
 template <class T>
-struct PassArgs {
+struct alignas(64) PassArgs {
+    CUtensorMap tmap;                 // PF == 3: strided input rows as a 3-D tensor
     const C<T>* in;
     C<T>* out;
     long long batch, sig_base, n;
@@ -90,19 +93,33 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // smem buffer with cp.async while tile i is transformed (the engine's
 // exchanges run in tile i's half), so HBM latency overlaps compute even at
 // one or two CTAs per SM.
+// 3-D tensor TMA load (SASS UTMALDG) of one box into shared memory
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                            unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+        "[%5];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<unsigned long long>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+        : "memory");
+}
+
 template <class T, int L, int E, int U, int P, int KIND, int ABFT, int MINB, int PF, class Radices>
 __global__ void __launch_bounds__(U * (L / E), MINB)
-fft_pass_kernel(const PassArgs<T> a) {
+fft_pass_kernel(const __grid_constant__ PassArgs<T> a) {
     constexpr int TPS = L / E;
     constexpr int THREADS = U * TPS;
     constexpr int RS = U + P;  // smem row stride (elements) of the [L][U] tile
     // PF = 2: per-row TMA bulk copies (cp.async.bulk, one instruction per row
     // segment, no per-element issue work) into a dense staging layout, two
     // buffers on two mbarriers. Rows of the last kind land at a padded stride.
-    constexpr bool BULK = PF == 2;
+    // PF = 3: like 2, but the strided kinds load whole [U x 256] boxes with one
+    // tensor-TMA instruction each (thread 0), the last kind keeps bulk rows.
+    constexpr bool BULK = PF == 2 || PF == 3;
+    constexpr bool TENSOR = PF == 3 && KIND != KIND_LAST;
+    constexpr int BOXR = L < 256 ? L : 256;
     constexpr int SU = sizeof(T) == 4 ? L + 2 : L + 1;  // 16-byte aligned padded row
     constexpr int BUFE = BULK ? (L * RS > U * SU ? L * RS : U * SU) : L * RS;
-    constexpr int ISSUERS = KIND == KIND_LAST ? U : (L < THREADS ? L : THREADS);
+    constexpr int ISSUERS = KIND == KIND_LAST ? U : (TENSOR ? 1 : (L < THREADS ? L : THREADS));
     using Eng = Engine<T, L, E, Radices>;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     C<T>* tile = reinterpret_cast<C<T>*>(smem_raw);
@@ -147,7 +164,14 @@ fft_pass_kernel(const PassArgs<T> a) {
         const long long h0 = v0 / a.lo_count, l0 = v0 - h0 * a.lo_count;
         const C<T>* sb = a.in + bb * a.n + h0 * a.in_hi + l0 * a.in_lo;
         fence_proxy_async();
-        if constexpr (KIND == KIND_LAST) {  // row u: L contiguous elements
+        if constexpr (TENSOR) {  // boxes of [U contiguous x BOXR strided rows]
+            constexpr int CW = sizeof(C<T>) / 4;  // 32-bit words per element
+            mbar_expect_tx(bar, L * U * sizeof(C<T>));
+            const int c2 = KIND == KIND_FIRST ? (int)bb : (int)(bb * (a.n / a.in_hi) + h0);
+#pragma unroll
+            for (int k = 0; k < L / BOXR; ++k)
+                tma_load_3d(buf + k * BOXR * U, &a.tmap, (int)(l0 * CW), k * BOXR, c2, bar);
+        } else if constexpr (KIND == KIND_LAST) {  // row u: L contiguous elements
             const unsigned bytes = L * sizeof(C<T>);
             mbar_expect_tx(bar, bytes);
             bulk_g2s(buf + threadIdx.x * SU, sb + (long long)threadIdx.x * a.in_lo, bytes, bar);
@@ -383,6 +407,7 @@ __global__ void __launch_bounds__(256) abft_finalize_kernel(const FinalArgs<T> a
 struct PassEntry {
     int logl;
     int variant;  // index into codegen.PASS_CANDIDATES[prec][logl]
+    int pf;       // 0 direct, 1 cp.async, 2 bulk rows, 3 tensor TMA (needs a tensor map)
     int e, u, p, threads, smem;
     const void* fn[3][3];  // [kind][abft]
 };

@@ -129,6 +129,52 @@ const PassEntry* pass_entry(int prec, int logl, int kind) {
 
 int kind_of(int k, int nst) { return k == 0 ? KIND_FIRST : (k == nst - 1 ? KIND_LAST : KIND_MID); }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    });
+    return fn;
+}
+
+// The strided rows of a first / middle stage as a 3-D tensor of 32-bit words:
+//   first : [c (R0 elems), j (d0), b (batch)]        element (b, j, c) at b n + j R0 + c
+//   middle: [c2 (d2 elems), j (d1), (b, k0) (B d0)]  element at (b d0 + k0) R0 + j d2 + c2
+// boxes of [U elements x min(L, 256) rows x 1].
+template <class T>
+int encode_rows_tmap(CUtensorMap* map, const void* base, int kind, long long n, long long batch, long long d0,
+                     long long d1, long long d2, int U, long long L) {
+    EncodeTiledFn fn = encode_fn();
+    if (!fn) return merr(TFFT_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    const long long cw = sizeof(C<T>) / 4;
+    const long long es = sizeof(C<T>);
+    const long long R0 = n / d0;
+    cuuint64_t dims[3], strides[2];
+    if (kind == KIND_FIRST) {
+        dims[0] = cw * R0; dims[1] = d0; dims[2] = batch;
+        strides[0] = R0 * es; strides[1] = n * es;
+    } else {
+        dims[0] = cw * d2; dims[1] = d1; dims[2] = batch * d0;
+        strides[0] = d2 * es; strides[1] = R0 * es;
+    }
+    cuuint32_t box[3] = {(cuuint32_t)(cw * U), (cuuint32_t)(L < 256 ? L : 256), 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, const_cast<void*>(base), dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return merr(TFFT_ECUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+    return TFFT_OK;
+}
+
 std::mutex occ_mu;
 std::map<const void*, int> occ;
 
@@ -281,6 +327,10 @@ int multi_launch_t(MultiPlan& mp, const MultiLaunch& m, cudaStream_t st) {
                     a.f_unit = k1 * d0 + k0; a.f_idx = (int)(e / (d0 * d1));
                 }
             }
+        }
+        if (pe[k]->pf == 3 && kind != KIND_LAST) {
+            int rc = encode_rows_tmap<T>(&a.tmap, a.in, kind, n, m.batch, d0, d1, d2, pe[k]->u, mp.d[k]);
+            if (rc) return rc;
         }
         int rc = launch_pass<T>(mp, pe[k], kind, abft_v, a, mp.num_sms, st);
         if (rc) return rc;
