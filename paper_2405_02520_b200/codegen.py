@@ -345,6 +345,7 @@ def pass_configs():
                 if c["pf"] in (2, 3):  # bulk staging: last-kind rows at a padded stride
                     su = l + 2 if prec == "fp32" else l + 1
                     bufe = max(bufe, u * su)
+                bufe = (bufe + 15) // 16 * 16  # keeps the second buffer 128-byte aligned
                 smem = nbuf * bufe * eb + 3 * (threads // 32 + 1) * (eb // 2)
                 out.append(dict(prec=prec, logl=logl, l=l, e=e, radices=radices, u=u, p=p,
                                 threads=threads, smem=smem, minb=c["minb"], pf=c["pf"], variant=vi))

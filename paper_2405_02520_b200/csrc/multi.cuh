@@ -118,7 +118,9 @@ fft_pass_kernel(const __grid_constant__ PassArgs<T> a) {
     constexpr bool TENSOR = PF == 3 && KIND != KIND_LAST;
     constexpr int BOXR = L < 256 ? L : 256;
     constexpr int SU = sizeof(T) == 4 ? L + 2 : L + 1;  // 16-byte aligned padded row
-    constexpr int BUFE = BULK ? (L * RS > U * SU ? L * RS : U * SU) : L * RS;
+    // buffer size rounded to 16 elements so the second buffer stays 128-byte
+    // aligned (tensor-TMA destination requirement)
+    constexpr int BUFE = ((BULK ? (L * RS > U * SU ? L * RS : U * SU) : L * RS) + 15) / 16 * 16;
     constexpr int ISSUERS = KIND == KIND_LAST ? U : (TENSOR ? 1 : (L < THREADS ? L : THREADS));
     using Eng = Engine<T, L, E, Radices>;
     extern __shared__ __align__(128) unsigned char smem_raw[];
