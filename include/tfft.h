@@ -105,6 +105,20 @@ int tfft_run_protected(tfft_plan *plan, const void *in, void *out, int64_t batch
                        const tfft_fault *fault, int inverse,
                        tfft_report *report, void *stream);
 
+/* Host-buffer variant of tfft_run_protected (the numpy path of
+ * abft/protected.py:63-166 and cli.py:62-64): `in`/`out` are HOST arrays of
+ * batch*n complex elements (pinned memory streams at full PCIe rate; pageable
+ * memory works through the driver's staging). The batch streams through a
+ * ring of device chunks (whole checksum groups) with H2D, the fused
+ * protected transform and D2H overlapped on three streams; the report is that
+ * of one call over the whole batch. etw/values are device arrays as above.
+ * Blocks until `out` and the report are complete. */
+int tfft_run_protected_host(tfft_plan *plan, const void *in, void *out, int64_t batch,
+                            int scheme, double delta, double abs_floor,
+                            const void *etw, const void *values,
+                            const tfft_fault *fault, int inverse,
+                            tfft_report *report, void *stream);
+
 /* The two halves of tfft_run_protected, for callers that queue several
  * protected transforms before reading their reports (one in-flight protected
  * call per plan): _launch enqueues the fused transform and the tiny

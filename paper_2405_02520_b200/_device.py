@@ -49,6 +49,24 @@ def to_device(x, np_dtype, device=None):
     return host.to(dev), True
 
 
+def is_host(x) -> bool:
+    return not is_device(x)
+
+
+def host_tensor(x, np_dtype) -> torch.Tensor:
+    """Contiguous CPU tensor of the plan dtype sharing memory with `x` when it
+    already has that dtype and layout (pinned CPU tensors stay pinned)."""
+    td = torch_dtype(np_dtype)
+    if isinstance(x, torch.Tensor):
+        return x.to(td).contiguous()
+    return torch.from_numpy(np.ascontiguousarray(np.asarray(x), dtype=np_dtype))
+
+
+def pinned_empty(shape, td) -> torch.Tensor:
+    """Pinned host tensor from torch's caching host allocator."""
+    return torch.empty(shape, dtype=td, pin_memory=True)
+
+
 def to_host(t: torch.Tensor) -> np.ndarray:
     """D2H into pinned memory from torch's caching host allocator (no page
     faulting of fresh pageable memory per call); the numpy array keeps the

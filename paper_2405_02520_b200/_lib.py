@@ -52,6 +52,8 @@ SIGNATURES = {
     "tfft_execute": (_INT, [_VP, _VP, _VP, _I64, _INT, _VP]),
     "tfft_run_protected": (_INT, [_VP, _VP, _VP, _I64, _INT, _DBL, _DBL, _VP, _VP,
                                   ctypes.POINTER(Fault), _INT, ctypes.POINTER(Report), _VP]),
+    "tfft_run_protected_host": (_INT, [_VP, _VP, _VP, _I64, _INT, _DBL, _DBL, _VP, _VP,
+                                       ctypes.POINTER(Fault), _INT, ctypes.POINTER(Report), _VP]),
     "tfft_protect_launch": (_INT, [_VP, _VP, _VP, _I64, _INT, _DBL, _DBL, _VP, _VP,
                                    ctypes.POINTER(Fault), _INT, ctypes.POINTER(Report), _VP]),
     "tfft_protect_finish": (_INT, [_VP, _VP, _VP, _I64, _INT, _DBL, _DBL, _VP, _VP, _INT,

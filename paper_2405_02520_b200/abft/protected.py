@@ -100,9 +100,12 @@ def _fault_struct(inj: BitFlipInjector) -> _lib.Fault | None:
     return f
 
 
-def _fused(plan, x, out, scheme, cfg, enc, inverse, injector):
+def _fused(plan, x, out, scheme, cfg, enc, inverse, injector, host=False):
+    """One C-ABI call: tfft_run_protected on device tensors, or (host=True)
+    tfft_run_protected_host streaming host tensors through the device."""
     lib = _lib.load()
-    h = native_plan(plan, x.device.index)
+    dev = torch.cuda.current_device() if host else x.device.index
+    h = native_plan(plan, dev)
     batch = x.shape[0]
     cap = max(16, min(batch, 1 << 16))
     flags = (_lib.Flag * cap)()
@@ -121,7 +124,8 @@ def _fused(plan, x, out, scheme, cfg, enc, inverse, injector):
     if scheme is not Scheme.NONE:
         row = enc.device_row(x.dtype, inverse)
         vals = enc.device_values(x.dtype)
-    _lib.check(lib.tfft_run_protected(
+    entry = lib.tfft_run_protected_host if host else lib.tfft_run_protected
+    _lib.check(entry(
         h.handle, x.data_ptr(), out.data_ptr(), batch, code, float(cfg.delta), float(cfg.abs_floor),
         _device.ptr(row), _device.ptr(vals), ctypes.byref(fault) if fault is not None else None,
         int(bool(inverse)), ctypes.byref(rep), _device.stream_ptr()), "tfft_run_protected")
@@ -206,13 +210,27 @@ def run_protected(plan: FftPlan, twiddles: TwiddleTable, batch, scheme=Scheme.TW
     """
     scheme = Scheme(scheme)
     check_backend(backend)
+    if cfg is None:
+        cfg = DetectionConfig(delta=default_delta(plan.precision))
+    if _device.is_host(batch) and (injector is None or isinstance(injector, BitFlipInjector)):
+        # host drop-in: H2D / fused transform / D2H streamed in chunks
+        _device.require_cuda()
+        xh = _device.host_tensor(batch, plan.dtype)
+        if xh.dim() != 2 or xh.shape[1] != plan.n:
+            raise ValueError("batch must have shape (B, n) with n == plan.n")
+        if xh.shape[0] % plan.bs:
+            raise ValueError(f"batch size {xh.shape[0]} not divisible by group size {plan.bs}")
+        if enc is None and scheme is not Scheme.NONE:
+            enc = make_encoding(EncodingKind.WANG, plan.n)
+        out = _device.pinned_empty(xh.shape, xh.dtype)
+        report = _fused(plan, xh, out, scheme, cfg, enc, inverse, injector, host=True)
+        counter = PassCounter(reads=report.pass_count // 2, writes=report.pass_count // 2)
+        return out.numpy(), report, counter
     x, host = _device.to_device(batch, plan.dtype)
     if x.dim() != 2 or x.shape[1] != plan.n:
         raise ValueError("batch must have shape (B, n) with n == plan.n")
     if x.shape[0] % plan.bs:
         raise ValueError(f"batch size {x.shape[0]} not divisible by group size {plan.bs}")
-    if cfg is None:
-        cfg = DetectionConfig(delta=default_delta(plan.precision))
     if enc is None and scheme is not Scheme.NONE:
         enc = make_encoding(EncodingKind.WANG, plan.n)
     out = torch.empty_like(x)

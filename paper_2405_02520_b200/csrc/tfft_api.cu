@@ -186,6 +186,13 @@ struct tfft_plan {
     FixJob* d_jobs = nullptr;
     int64_t jobs_cap = 0;
     cudaEvent_t ev_done = nullptr;  // detection summary landed in h_cnt
+    // host-streaming path (tfft_run_protected_host): a ring of device chunk
+    // buffers, copy streams for each direction, per-slot events
+    static constexpr int kRing = 3;
+    cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+    void* ring = nullptr;           // kRing x (in chunk, out chunk)
+    size_t ring_chunk = 0;          // bytes of one chunk buffer
+    cudaEvent_t ev_in[kRing] = {}, ev_comp[kRing] = {}, ev_out[kRing] = {};
 };
 
 namespace {
@@ -312,6 +319,79 @@ int check_plan(tfft_plan* p) {
     return TFFT_OK;
 }
 
+// Validation, report reset and the fault translated into launch coordinates
+// (shared by the device and the host-streaming entry points).
+int prepare_protected(tfft_plan* p, const void* in, void* out, int64_t batch, int scheme, double delta,
+                      const void* etw, const void* values, double abs_floor, const tfft_fault* fault, int inverse,
+                      tfft_report* rep, Launch& L) {
+    if (!rep) return fail(TFFT_EINVAL, "null report");
+    if (batch < 1 || !in || !out) return fail(TFFT_EINVAL, "batch must have shape (B, n) with n == plan.n");
+    if (batch % p->bs) return fail(TFFT_EINVAL, "batch size not divisible by group size");
+    if (scheme < TFFT_SCHEME_NONE || scheme > TFFT_SCHEME_TWO_SIDED_GROUP) return fail(TFFT_EINVAL, "bad scheme");
+    const bool prot = scheme != TFFT_SCHEME_NONE;
+    if (prot && !etw) return fail(TFFT_EINVAL, "protected schemes need the encoding row");
+    if (prot && !(delta > 0)) return fail(TFFT_EINVAL, "delta must be positive");
+    const int64_t groups = batch / p->bs;
+    const int64_t n = p->n;
+    rep->groups = groups;
+    rep->recompute_count = 0;
+    rep->pass_count = 2 * (int64_t)p->nstages * groups;
+    rep->max_rel_discrepancy = 0.0;
+    rep->n_flagged = rep->n_corrected = rep->n_unrecoverable = 0;
+    rep->fault_fired = 0;
+
+    L = base_launch(in, out, batch, inverse ? 1 : 0);
+    L.abft = prot ? (values ? ABFT_TABLE : ABFT_WANG) : ABFT_OFF;
+    L.etw = etw;
+    L.values = values;
+    L.delta = delta;
+    L.abs_floor = abs_floor;
+    // ---- translate the fault into the launch's coordinates
+    if (fault && fault->where != TFFT_AT_NONE) {
+        const int width = p->prec == TFFT_FP32 ? 32 : 64;
+        bool fires = fault->signal >= 0 && fault->signal < batch && fault->element >= 0 && fault->element < n;
+        if (fault->where == TFFT_AT_STAGE && (fault->stage < 0 || fault->stage >= p->nstages)) fires = false;
+        if (fires) {
+            if (fault->bit < 0 || fault->bit >= width) return fail(TFFT_EINVAL, "bit out of range for the precision");
+            if (fault->component != 0 && fault->component != 1) return fail(TFFT_EINVAL, "component must be re/im");
+            L.f_signal = fault->signal;
+            L.f_comp = fault->component;
+            L.f_bit = fault->bit;
+            L.f_stage = fault->stage;
+            if (p->single) {
+                if (fault->where == TFFT_AT_INPUT) {
+                    L.f_where = AT_INPUT;
+                    L.f_elem = fault->element;
+                } else if (fault->where == TFFT_AT_OUTPUT) {
+                    L.f_where = AT_OUTPUT;
+                    L.f_elem = fault->element;
+                } else {
+                    if (fault->stage != p->nstages - 1)
+                        return fail(TFFT_EUNSUPPORTED, "intermediate-stage injection needs a multi-pass size");
+                    // last-stage hook index -> natural order (SURVEY section 7)
+                    const int64_t e = fault->element;
+                    int64_t f = e;
+                    if (p->nstages == 2) {
+                        const int64_t d0 = p->dims[0], d1 = p->dims[1];
+                        f = (e / d1) + d0 * (e % d1);
+                    } else if (p->nstages == 3) {
+                        const int64_t d0 = p->dims[0], d1 = p->dims[1], d2 = p->dims[2];
+                        const int64_t k0 = e / (d1 * d2), k1 = (e / d2) % d1, k2 = e % d2;
+                        f = k0 + d0 * k1 + d0 * d1 * k2;
+                    }
+                    L.f_where = AT_PRESCALE;
+                    L.f_elem = f;
+                }
+            } else {
+                L.f_where = fault->where == TFFT_AT_INPUT ? 1 : (fault->where == TFFT_AT_STAGE ? 2 : 3);
+                L.f_elem = fault->element;
+            }
+            rep->fault_fired = 1;
+        }
+    }
+    return TFFT_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -412,6 +492,14 @@ int tfft_plan_destroy(tfft_plan* p) {
     cudaFree(p->d_scratch);
     cudaFree(p->d_jobs);
     if (p->ev_done) cudaEventDestroy(p->ev_done);
+    cudaFree(p->ring);
+    for (int i = 0; i < tfft_plan::kRing; ++i) {
+        if (p->ev_in[i]) cudaEventDestroy(p->ev_in[i]);
+        if (p->ev_comp[i]) cudaEventDestroy(p->ev_comp[i]);
+        if (p->ev_out[i]) cudaEventDestroy(p->ev_out[i]);
+    }
+    if (p->s_h2d) cudaStreamDestroy(p->s_h2d);
+    if (p->s_d2h) cudaStreamDestroy(p->s_d2h);
     delete p;
     return TFFT_OK;
 }
@@ -548,71 +636,10 @@ int tfft_protect_launch(tfft_plan* p, const void* in, void* out, int64_t batch, 
     int rc = check_plan(p);
     if (rc) return rc;
     cudaStream_t st = (cudaStream_t)stream;
-    if (!rep) return fail(TFFT_EINVAL, "null report");
-    if (batch < 1 || !in || !out) return fail(TFFT_EINVAL, "batch must have shape (B, n) with n == plan.n");
-    if (batch % p->bs) return fail(TFFT_EINVAL, "batch size not divisible by group size");
-    if (scheme < TFFT_SCHEME_NONE || scheme > TFFT_SCHEME_TWO_SIDED_GROUP) return fail(TFFT_EINVAL, "bad scheme");
+    Launch L;
+    rc = prepare_protected(p, in, out, batch, scheme, delta, etw, values, abs_floor, fault, inverse, rep, L);
+    if (rc) return rc;
     const bool prot = scheme != TFFT_SCHEME_NONE;
-    if (prot && !etw) return fail(TFFT_EINVAL, "protected schemes need the encoding row");
-    if (prot && !(delta > 0)) return fail(TFFT_EINVAL, "delta must be positive");
-    const int64_t groups = batch / p->bs;
-    const int64_t n = p->n;
-    rep->groups = groups;
-    rep->recompute_count = 0;
-    rep->pass_count = 2 * (int64_t)p->nstages * groups;
-    rep->max_rel_discrepancy = 0.0;
-    rep->n_flagged = rep->n_corrected = rep->n_unrecoverable = 0;
-    rep->fault_fired = 0;
-
-    Launch L = base_launch(in, out, batch, inverse ? 1 : 0);
-    L.abft = prot ? (values ? ABFT_TABLE : ABFT_WANG) : ABFT_OFF;
-    L.etw = etw;
-    L.values = values;
-    L.delta = delta;
-    L.abs_floor = abs_floor;
-    // ---- translate the fault into the launch's coordinates
-    if (fault && fault->where != TFFT_AT_NONE) {
-        const int width = p->prec == TFFT_FP32 ? 32 : 64;
-        bool fires = fault->signal >= 0 && fault->signal < batch && fault->element >= 0 && fault->element < n;
-        if (fault->where == TFFT_AT_STAGE && (fault->stage < 0 || fault->stage >= p->nstages)) fires = false;
-        if (fires) {
-            if (fault->bit < 0 || fault->bit >= width) return fail(TFFT_EINVAL, "bit out of range for the precision");
-            if (fault->component != 0 && fault->component != 1) return fail(TFFT_EINVAL, "component must be re/im");
-            L.f_signal = fault->signal;
-            L.f_comp = fault->component;
-            L.f_bit = fault->bit;
-            L.f_stage = fault->stage;
-            if (p->single) {
-                if (fault->where == TFFT_AT_INPUT) {
-                    L.f_where = AT_INPUT;
-                    L.f_elem = fault->element;
-                } else if (fault->where == TFFT_AT_OUTPUT) {
-                    L.f_where = AT_OUTPUT;
-                    L.f_elem = fault->element;
-                } else {
-                    if (fault->stage != p->nstages - 1)
-                        return fail(TFFT_EUNSUPPORTED, "intermediate-stage injection needs a multi-pass size");
-                    // last-stage hook index -> natural order (SURVEY section 7)
-                    const int64_t e = fault->element;
-                    int64_t f = e;
-                    if (p->nstages == 2) {
-                        const int64_t d0 = p->dims[0], d1 = p->dims[1];
-                        f = (e / d1) + d0 * (e % d1);
-                    } else if (p->nstages == 3) {
-                        const int64_t d0 = p->dims[0], d1 = p->dims[1], d2 = p->dims[2];
-                        const int64_t k0 = e / (d1 * d2), k1 = (e / d2) % d1, k2 = e % d2;
-                        f = k0 + d0 * k1 + d0 * d1 * k2;
-                    }
-                    L.f_where = AT_PRESCALE;
-                    L.f_elem = f;
-                }
-            } else {
-                L.f_where = fault->where == TFFT_AT_INPUT ? 1 : (fault->where == TFFT_AT_STAGE ? 2 : 3);
-                L.f_elem = fault->element;
-            }
-            rep->fault_fired = 1;
-        }
-    }
     if (prot) {
         rc = ensure_flags(p, batch);
         if (rc) return rc;
@@ -628,16 +655,15 @@ int tfft_protect_launch(tfft_plan* p, const void* in, void* out, int64_t batch, 
     return TFFT_OK;
 }
 
-int tfft_protect_finish(tfft_plan* p, const void* in, void* out, int64_t batch, int scheme, double delta,
-                        double abs_floor, const void* etw, const void* values, int inverse, tfft_report* rep,
-                        void* stream) {
-    int rc = check_plan(p);
-    if (rc) return rc;
-    cudaStream_t st = (cudaStream_t)stream;
-    if (!rep) return fail(TFFT_EINVAL, "null report");
-    if (scheme == TFFT_SCHEME_NONE) return TFFT_OK;
-    if (!p->ev_done) return fail(TFFT_EINVAL, "tfft_protect_finish without tfft_protect_launch");
-    const int64_t n = p->n;
+}  // extern "C"
+
+namespace {
+
+// Detection summary of the launches since the last counter reset: max rel
+// discrepancy and the flagged (global signal, rel) list, sorted like the
+// reference's group loop.
+int read_summary(tfft_plan* p, int64_t batch, cudaStream_t st, tfft_report* rep,
+                 std::vector<std::pair<long long, double>>& flags) {
     CU(cudaEventSynchronize(p->ev_done));
     const int64_t nflag = std::min<int64_t>(p->h_cnt->flag_count, batch);
     if (p->prec == TFFT_FP32) {
@@ -650,7 +676,7 @@ int tfft_protect_finish(tfft_plan* p, const void* in, void* out, int64_t batch, 
         memcpy(&d, &p->h_cnt->max_key, 8);
         rep->max_rel_discrepancy = d;
     }
-    std::vector<std::pair<long long, double>> flags;
+    flags.clear();
     if (nflag > 0) {
         std::vector<long long> sig(nflag);
         CU(cudaMemcpyAsync(sig.data(), p->d_flag_sig, nflag * sizeof(long long), cudaMemcpyDeviceToHost, st));
@@ -674,8 +700,13 @@ int tfft_protect_finish(tfft_plan* p, const void* in, void* out, int64_t batch, 
         rep->flagged[i].signal = flags[i].first;
         rep->flagged[i].discrepancy = flags[i].second;
     }
-    // group decisions
-    std::vector<int64_t> bad_groups, fix_groups, fix_sig;
+    return TFFT_OK;
+}
+
+// Group decisions (protected.py:127-136): more than one flag in a group ->
+// unrecoverable, exactly one -> a correction candidate.
+void decide(const tfft_plan* p, const std::vector<std::pair<long long, double>>& flags,
+            std::vector<int64_t>& bad_groups, std::vector<int64_t>& fix_groups, std::vector<int64_t>& fix_sig) {
     for (size_t i = 0; i < flags.size();) {
         const int64_t g = flags[i].first / p->bs;
         size_t j = i;
@@ -684,71 +715,88 @@ int tfft_protect_finish(tfft_plan* p, const void* in, void* out, int64_t batch, 
         else { fix_groups.push_back(g); fix_sig.push_back(flags[i].first); }
         i = j;
     }
-    std::vector<char> fixed_ok(fix_groups.size(), 0);
-    if (!fix_groups.empty()) {
-        if (scheme == TFFT_SCHEME_ONE_SIDED) {
-            // time redundancy: re-transform the flagged signal from the clean input
-            for (size_t i = 0; i < fix_groups.size(); ++i) {
-                Launch R = base_launch((const char*)in + fix_sig[i] * n * p->esize,
-                                       (char*)out + fix_sig[i] * n * p->esize, 1, inverse ? 1 : 0);
-                rc = launch_transform(p, R, st);
-                if (rc) return rc;
-                fixed_ok[i] = 1;
-            }
-            rep->recompute_count = (int64_t)fix_groups.size();
-            rep->pass_count += 2 * (int64_t)p->nstages * rep->recompute_count;
-        } else {
-            // two-sided: y_f = W s0 - sum_{b != f} y_b, verified before commit
-            const int64_t chunk_max = std::max<int64_t>(1, std::min<int64_t>(256, (int64_t(1) << 28) / (n * (int64_t)p->esize)));
-            for (size_t c0 = 0; c0 < fix_groups.size(); c0 += chunk_max) {
-                const int64_t K = std::min<int64_t>(chunk_max, fix_groups.size() - c0);
-                rc = ensure_scratch(p, (size_t)3 * K * n * p->esize);
-                if (rc) return rc;
-                char* s0 = (char*)p->d_scratch;
-                char* ws0 = s0 + (size_t)K * n * p->esize;
-                char* fx = ws0 + (size_t)K * n * p->esize;
-                if (K > p->jobs_cap) {
-                    cudaFree(p->d_jobs);
-                    p->d_jobs = nullptr;
-                    CU(cudaMalloc(&p->d_jobs, K * sizeof(FixJob)));
-                    p->jobs_cap = K;
-                }
-                std::vector<FixJob> jobs(K);
-                const int grid = (int)std::min<long long>((n + 255) / 256, 4LL * p->num_sms);
-                for (int64_t k = 0; k < K; ++k) {
-                    const int64_t g = fix_groups[c0 + k];
-                    jobs[k].first = g * p->bs;
-                    jobs[k].flagged = fix_sig[c0 + k];
-                    jobs[k].ok = 0;
-                    const char* xg = (const char*)in + (size_t)g * p->bs * n * p->esize;
-                    if (p->prec == TFFT_FP32)
-                        group_sums_kernel<float><<<grid, 256, 0, st>>>((const float2*)xg, p->bs, n,
-                                                                       (float2*)(s0 + k * n * p->esize), nullptr);
-                    else
-                        group_sums_kernel<double><<<grid, 256, 0, st>>>((const double2*)xg, p->bs, n,
-                                                                        (double2*)(s0 + k * n * p->esize), nullptr);
-                }
-                CU(cudaGetLastError());
-                Launch W = base_launch(s0, ws0, K, inverse ? 1 : 0);
-                rc = launch_transform(p, W, st);
-                if (rc) return rc;
-                CU(cudaMemcpyAsync(p->d_jobs, jobs.data(), K * sizeof(FixJob), cudaMemcpyHostToDevice, st));
-                if (p->prec == TFFT_FP32)
-                    fix_groups_kernel<float><<<(unsigned)K, AUX_THREADS, 0, st>>>(
-                        (const float2*)in, (float2*)out, n, p->bs, (const float2*)ws0, (float2*)fx,
-                        (const float2*)etw, (const float2*)values, (float)delta, (float)abs_floor, 1e-6f, p->d_jobs);
-                else
-                    fix_groups_kernel<double><<<(unsigned)K, AUX_THREADS, 0, st>>>(
-                        (const double2*)in, (double2*)out, n, p->bs, (const double2*)ws0, (double2*)fx,
-                        (const double2*)etw, (const double2*)values, delta, abs_floor, 1e-12, p->d_jobs);
-                CU(cudaGetLastError());
-                CU(cudaMemcpyAsync(jobs.data(), p->d_jobs, K * sizeof(FixJob), cudaMemcpyDeviceToHost, st));
-                CU(cudaStreamSynchronize(st));
-                for (int64_t k = 0; k < K; ++k) fixed_ok[c0 + k] = (char)jobs[k].ok;
-            }
+}
+
+// Correct the candidate groups of device buffers in/out (groups and signals
+// indexed relative to `in`). ONE_SIDED re-transforms the flagged signal from
+// the clean input (protected.py:142-147); TWO_SIDED_* rebuilds
+// y_f = W s0 - sum_{b != f} y_b and commits only if it re-verifies
+// (pipeline.py:164-192). fixed_ok[i] = 1 when group i was corrected.
+int correct_groups(tfft_plan* p, const void* in, void* out, int scheme, const void* etw, const void* values,
+                   double delta, double abs_floor, int inverse, const std::vector<int64_t>& fix_groups,
+                   const std::vector<int64_t>& fix_sig, std::vector<char>& fixed_ok, cudaStream_t st) {
+    const int64_t n = p->n;
+    int rc;
+    fixed_ok.assign(fix_groups.size(), 0);
+    if (fix_groups.empty()) return TFFT_OK;
+    if (scheme == TFFT_SCHEME_ONE_SIDED) {
+        for (size_t i = 0; i < fix_groups.size(); ++i) {
+            Launch R = base_launch((const char*)in + fix_sig[i] * n * p->esize,
+                                   (char*)out + fix_sig[i] * n * p->esize, 1, inverse ? 1 : 0);
+            rc = launch_transform(p, R, st);
+            if (rc) return rc;
+            fixed_ok[i] = 1;
         }
+        return TFFT_OK;
     }
-    // corrected / unrecoverable lists in group order
+    const int64_t chunk_max = std::max<int64_t>(1, std::min<int64_t>(256, (int64_t(1) << 28) / (n * (int64_t)p->esize)));
+    for (size_t c0 = 0; c0 < fix_groups.size(); c0 += chunk_max) {
+        const int64_t K = std::min<int64_t>(chunk_max, fix_groups.size() - c0);
+        rc = ensure_scratch(p, (size_t)3 * K * n * p->esize);
+        if (rc) return rc;
+        char* s0 = (char*)p->d_scratch;
+        char* ws0 = s0 + (size_t)K * n * p->esize;
+        char* fx = ws0 + (size_t)K * n * p->esize;
+        if (K > p->jobs_cap) {
+            cudaFree(p->d_jobs);
+            p->d_jobs = nullptr;
+            CU(cudaMalloc(&p->d_jobs, K * sizeof(FixJob)));
+            p->jobs_cap = K;
+        }
+        std::vector<FixJob> jobs(K);
+        const int grid = (int)std::min<long long>((n + 255) / 256, 4LL * p->num_sms);
+        for (int64_t k = 0; k < K; ++k) {
+            const int64_t g = fix_groups[c0 + k];
+            jobs[k].first = g * p->bs;
+            jobs[k].flagged = fix_sig[c0 + k];
+            jobs[k].ok = 0;
+            const char* xg = (const char*)in + (size_t)g * p->bs * n * p->esize;
+            if (p->prec == TFFT_FP32)
+                group_sums_kernel<float><<<grid, 256, 0, st>>>((const float2*)xg, p->bs, n,
+                                                               (float2*)(s0 + k * n * p->esize), nullptr);
+            else
+                group_sums_kernel<double><<<grid, 256, 0, st>>>((const double2*)xg, p->bs, n,
+                                                                (double2*)(s0 + k * n * p->esize), nullptr);
+        }
+        CU(cudaGetLastError());
+        Launch W = base_launch(s0, ws0, K, inverse ? 1 : 0);
+        rc = launch_transform(p, W, st);
+        if (rc) return rc;
+        CU(cudaMemcpyAsync(p->d_jobs, jobs.data(), K * sizeof(FixJob), cudaMemcpyHostToDevice, st));
+        if (p->prec == TFFT_FP32)
+            fix_groups_kernel<float><<<(unsigned)K, AUX_THREADS, 0, st>>>(
+                (const float2*)in, (float2*)out, n, p->bs, (const float2*)ws0, (float2*)fx,
+                (const float2*)etw, (const float2*)values, (float)delta, (float)abs_floor, 1e-6f, p->d_jobs);
+        else
+            fix_groups_kernel<double><<<(unsigned)K, AUX_THREADS, 0, st>>>(
+                (const double2*)in, (double2*)out, n, p->bs, (const double2*)ws0, (double2*)fx,
+                (const double2*)etw, (const double2*)values, delta, abs_floor, 1e-12, p->d_jobs);
+        CU(cudaGetLastError());
+        CU(cudaMemcpyAsync(jobs.data(), p->d_jobs, K * sizeof(FixJob), cudaMemcpyDeviceToHost, st));
+        CU(cudaStreamSynchronize(st));
+        for (int64_t k = 0; k < K; ++k) fixed_ok[c0 + k] = (char)jobs[k].ok;
+    }
+    return TFFT_OK;
+}
+
+// corrected / unrecoverable lists in group order; recompute accounting
+void fill_lists(tfft_plan* p, int scheme, tfft_report* rep, const std::vector<int64_t>& bad_groups,
+                const std::vector<int64_t>& fix_groups, const std::vector<int64_t>& fix_sig,
+                const std::vector<char>& fixed_ok) {
+    if (scheme == TFFT_SCHEME_ONE_SIDED && !fix_groups.empty()) {
+        rep->recompute_count = (int64_t)fix_groups.size();
+        rep->pass_count += 2 * (int64_t)p->nstages * rep->recompute_count;
+    }
     std::vector<int64_t> unrec = bad_groups;
     int64_t nc = 0;
     for (size_t i = 0; i < fix_groups.size(); ++i) {
@@ -766,6 +814,30 @@ int tfft_protect_finish(tfft_plan* p, const void* in, void* out, int64_t batch, 
     rep->n_corrected = nc;
     rep->n_unrecoverable = (int64_t)unrec.size();
     for (size_t i = 0; i < unrec.size() && (int64_t)i < rep->unrecoverable_cap; ++i) rep->unrecoverable[i] = unrec[i];
+}
+
+}  // namespace
+
+extern "C" {
+
+int tfft_protect_finish(tfft_plan* p, const void* in, void* out, int64_t batch, int scheme, double delta,
+                        double abs_floor, const void* etw, const void* values, int inverse, tfft_report* rep,
+                        void* stream) {
+    int rc = check_plan(p);
+    if (rc) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (!rep) return fail(TFFT_EINVAL, "null report");
+    if (scheme == TFFT_SCHEME_NONE) return TFFT_OK;
+    if (!p->ev_done) return fail(TFFT_EINVAL, "tfft_protect_finish without tfft_protect_launch");
+    std::vector<std::pair<long long, double>> flags;
+    rc = read_summary(p, batch, st, rep, flags);
+    if (rc) return rc;
+    std::vector<int64_t> bad_groups, fix_groups, fix_sig;
+    decide(p, flags, bad_groups, fix_groups, fix_sig);
+    std::vector<char> fixed_ok;
+    rc = correct_groups(p, in, out, scheme, etw, values, delta, abs_floor, inverse, fix_groups, fix_sig, fixed_ok, st);
+    if (rc) return rc;
+    fill_lists(p, scheme, rep, bad_groups, fix_groups, fix_sig, fixed_ok);
     return TFFT_OK;
 }
 
@@ -833,6 +905,123 @@ int tfft_tile_fft(const void* in, void* out, int64_t t, int64_t l, int dtype_byt
         CU(cudaMemcpyAsync(out, dout, bytes, cudaMemcpyDeviceToHost, st));
         CU(cudaStreamSynchronize(st));
     }
+    return TFFT_OK;
+}
+
+// Host-buffer drop-in of run_protected (the numpy path of the reference,
+// protected.py:63-166): the batch streams through a ring of device chunks —
+// H2D of chunk i+1, the fused protected transform of chunk i and D2H of chunk
+// i-1 run concurrently on three streams. Chunks are whole checksum groups and
+// keep their global signal indices (sig_base), so flags, the fault and the
+// report are those of one call over the whole batch. Flagged groups (rare)
+// are re-staged afterwards and corrected on the device like the device path.
+int tfft_run_protected_host(tfft_plan* p, const void* in, void* out, int64_t batch, int scheme, double delta,
+                            double abs_floor, const void* etw, const void* values, const tfft_fault* fault,
+                            int inverse, tfft_report* rep, void* stream) {
+    int rc = check_plan(p);
+    if (rc) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    Launch L;
+    rc = prepare_protected(p, in, out, batch, scheme, delta, etw, values, abs_floor, fault, inverse, rep, L);
+    if (rc) return rc;
+    const bool prot = scheme != TFFT_SCHEME_NONE;
+    const size_t sig_bytes = (size_t)p->n * p->esize;
+    const size_t grp_bytes = sig_bytes * p->bs;
+    // ~32 MiB chunks (whole groups): deep enough to hide launch gaps, small
+    // enough that the pipeline fill/drain is a few percent of a 1 GiB batch
+    const int64_t target = (int64_t)1 << 25;
+    int64_t gpc = std::max<int64_t>(1, target / (int64_t)grp_bytes);
+    gpc = std::min<int64_t>(gpc, batch / p->bs);
+    const size_t chunk = (size_t)gpc * grp_bytes;
+    if (!p->s_h2d) {
+        CU(cudaStreamCreateWithFlags(&p->s_h2d, cudaStreamNonBlocking));
+        CU(cudaStreamCreateWithFlags(&p->s_d2h, cudaStreamNonBlocking));
+        for (int i = 0; i < tfft_plan::kRing; ++i) {
+            CU(cudaEventCreateWithFlags(&p->ev_in[i], cudaEventDisableTiming));
+            CU(cudaEventCreateWithFlags(&p->ev_comp[i], cudaEventDisableTiming));
+            CU(cudaEventCreateWithFlags(&p->ev_out[i], cudaEventDisableTiming));
+        }
+    }
+    if (!p->ev_done) CU(cudaEventCreateWithFlags(&p->ev_done, cudaEventDisableTiming));
+    if (chunk > p->ring_chunk) {
+        CU(cudaStreamSynchronize(st));
+        CU(cudaStreamSynchronize(p->s_h2d));
+        CU(cudaStreamSynchronize(p->s_d2h));
+        cudaFree(p->ring);
+        p->ring = nullptr;
+        p->ring_chunk = 0;
+        if (cudaMalloc(&p->ring, 2 * tfft_plan::kRing * chunk) != cudaSuccess)
+            return fail(TFFT_ENOMEM, "host-streaming ring");
+        p->ring_chunk = chunk;
+    }
+    if (prot) {
+        rc = ensure_flags(p, batch);
+        if (rc) return rc;
+        CU(cudaMemsetAsync(p->d_cnt, 0, sizeof(Counters), st));
+    }
+    // the copy streams start behind whatever the caller queued on `st`
+    CU(cudaEventRecord(p->ev_done, st));
+    CU(cudaStreamWaitEvent(p->s_h2d, p->ev_done, 0));
+    CU(cudaStreamWaitEvent(p->s_d2h, p->ev_done, 0));
+    const int64_t spc = gpc * p->bs;  // signals per chunk
+    const int64_t nchunks = (batch + spc - 1) / spc;
+    for (int64_t c = 0; c < nchunks; ++c) {
+        const int slot = (int)(c % tfft_plan::kRing);
+        char* din = (char*)p->ring + (size_t)slot * 2 * p->ring_chunk;
+        char* dout = din + p->ring_chunk;
+        const int64_t s0 = c * spc;
+        const int64_t ns = std::min<int64_t>(spc, batch - s0);
+        const size_t bytes = (size_t)ns * sig_bytes;
+        if (c >= tfft_plan::kRing) {  // slot reuse: its last transform and D2H are done
+            CU(cudaStreamWaitEvent(p->s_h2d, p->ev_comp[slot], 0));
+        }
+        CU(cudaMemcpyAsync(din, (const char*)in + s0 * sig_bytes, bytes, cudaMemcpyHostToDevice, p->s_h2d));
+        CU(cudaEventRecord(p->ev_in[slot], p->s_h2d));
+        CU(cudaStreamWaitEvent(st, p->ev_in[slot], 0));
+        if (c >= tfft_plan::kRing) CU(cudaStreamWaitEvent(st, p->ev_out[slot], 0));
+        Launch C = L;
+        C.in = din;
+        C.out = dout;
+        C.batch = ns;
+        C.sig_base = s0;
+        rc = launch_transform(p, C, st);
+        if (rc) return rc;
+        CU(cudaEventRecord(p->ev_comp[slot], st));
+        CU(cudaStreamWaitEvent(p->s_d2h, p->ev_comp[slot], 0));
+        CU(cudaMemcpyAsync((char*)out + s0 * sig_bytes, dout, bytes, cudaMemcpyDeviceToHost, p->s_d2h));
+        CU(cudaEventRecord(p->ev_out[slot], p->s_d2h));
+    }
+    // join: `st` waits for the last D2H so callers may sync on their stream
+    CU(cudaEventRecord(p->ev_out[0], p->s_d2h));
+    CU(cudaStreamWaitEvent(st, p->ev_out[0], 0));
+    if (!prot) return cudaStreamSynchronize(st) == cudaSuccess ? TFFT_OK : fail(TFFT_ECUDA, "stream sync");
+    CU(cudaMemcpyAsync(p->h_cnt, p->d_cnt, sizeof(Counters), cudaMemcpyDeviceToHost, st));
+    CU(cudaEventRecord(p->ev_done, st));
+    CU(cudaStreamSynchronize(st));
+    std::vector<std::pair<long long, double>> flags;
+    rc = read_summary(p, batch, st, rep, flags);
+    if (rc) return rc;
+    std::vector<int64_t> bad_groups, fix_groups, fix_sig;
+    decide(p, flags, bad_groups, fix_groups, fix_sig);
+    std::vector<char> fixed_ok(fix_groups.size(), 0);
+    // rare path: re-stage each candidate group (clean input + current output)
+    // into ring slot 0 and correct it there
+    char* din = (char*)p->ring;
+    char* dout = din + p->ring_chunk;
+    for (size_t i = 0; i < fix_groups.size(); ++i) {
+        const int64_t g = fix_groups[i];
+        const size_t off = (size_t)g * grp_bytes;
+        CU(cudaMemcpyAsync(din, (const char*)in + off, grp_bytes, cudaMemcpyHostToDevice, st));
+        CU(cudaMemcpyAsync(dout, (const char*)out + off, grp_bytes, cudaMemcpyHostToDevice, st));
+        std::vector<int64_t> g1{0}, s1{fix_sig[i] - g * p->bs};
+        std::vector<char> ok1;
+        rc = correct_groups(p, din, dout, scheme, etw, values, delta, abs_floor, inverse, g1, s1, ok1, st);
+        if (rc) return rc;
+        if (ok1[0]) CU(cudaMemcpyAsync((char*)out + off, dout, grp_bytes, cudaMemcpyDeviceToHost, st));
+        CU(cudaStreamSynchronize(st));
+        fixed_ok[i] = ok1[0];
+    }
+    fill_lists(p, scheme, rep, bad_groups, fix_groups, fix_sig, fixed_ok);
     return TFFT_OK;
 }
 

@@ -237,3 +237,28 @@ def test_zero_signals_flag_without_floor():
     _, rep2, _ = run_protected(plan, build_twiddles(plan), x, Scheme.TWO_SIDED_GROUP,
                                DetectionConfig(delta=1e-4, abs_floor=1e-12))
     assert rep2.flagged == []
+
+
+@pytest.mark.parametrize("n,prec,batch", [(1024, "fp32", 10000), (1 << 16, "fp64", 48), (64, "fp32", 16)])
+@pytest.mark.parametrize("scheme", ["two_sided_group", "one_sided", "none"])
+def test_host_streaming_matches_device_path(n, prec, batch, scheme):
+    """tfft_run_protected_host (numpy in -> numpy out, chunked H2D / transform /
+    D2H on three streams) gives the device path's outputs bit for bit and the
+    same report, with the fault landing in the last chunk."""
+    dt = np.complex64 if prec == "fp32" else np.complex128
+    x = random_batch(np.random.default_rng(7), (batch, n), dt)
+    plan = fit_group_size(make_plan(n, prec, batch=batch), batch)
+    tw = build_twiddles(plan)
+    cfg = DetectionConfig(delta=1e-4 if prec == "fp32" else 1e-9)
+    spec = FaultSpec(0, batch - 3, n // 3, "re", 30 if prec == "fp32" else 62)
+    yd, rd, cd = run_protected(plan, tw, torch.from_numpy(x).cuda(), scheme, cfg,
+                               injector=BitFlipInjector(spec))
+    inj = BitFlipInjector(spec)
+    yh, rh, ch = run_protected(plan, tw, x, scheme, cfg, injector=inj)
+    assert isinstance(yh, np.ndarray) and yh.dtype == x.dtype
+    assert np.array_equal(yh.view(np.uint8), yd.cpu().numpy().view(np.uint8))
+    assert rh.to_json() == rd.to_json()
+    assert ch.total == cd.total
+    assert inj.fired
+    if scheme != "none":
+        assert [c["signal"] for c in rh.corrected] == [batch - 3]

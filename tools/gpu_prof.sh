@@ -1,0 +1,12 @@
+# ncu --set full captures of single kernels, ABFT on vs off (usage: bash tools/gpu_prof.sh TAG "prec:logn ..." )
+set -x
+cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
+TAG=$1; shift
+for spec in $@; do
+  p=${spec%%:*}; l=${spec##*:}
+  for sc in two_sided_group none; do
+    timeout 600 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:"${KRE:-fft_single_kernel<float}" -s 1 -c 1 \
+      -o gpurun_out/${TAG}_${p}_n${l}_${sc} -f python tools/profile_single.py --prec $p --logn $l --scheme $sc --reps 2 > gpurun_out/${TAG}_${p}_n${l}_${sc}.log 2>&1
+  done
+done
+ls -la gpurun_out
