@@ -119,6 +119,22 @@ int tfft_run_protected_host(tfft_plan *plan, const void *in, void *out, int64_t 
                             const tfft_fault *fault, int inverse,
                             tfft_report *report, void *stream);
 
+/* Batched fault-injection campaign (fault_lab/campaign.py:95-195, the run
+ * loop of run_campaign): `runs` independent run_protected calls of
+ * `run_batch` signals each (in/out: device arrays of runs*run_batch*n
+ * elements, run r at rows r*run_batch...), fused into ONE protected launch.
+ * faults[r] is run r's single fault with a run-relative signal index
+ * (where == TFFT_AT_NONE for a clean run); faults may be NULL. Outputs:
+ * run_max_rel[r] (host, runs doubles) = run r's report.max_rel_discrepancy;
+ * run_fired[r] (host, may be NULL) = whether run r's fault fired; the report
+ * aggregates flags / corrections / unrecoverable groups with global indices
+ * (groups never span runs). Blocks until done. */
+int tfft_run_campaign(tfft_plan *plan, const void *in, void *out, int64_t runs,
+                      int64_t run_batch, int scheme, double delta, double abs_floor,
+                      const void *etw, const void *values, const tfft_fault *faults,
+                      int inverse, double *run_max_rel, int32_t *run_fired,
+                      tfft_report *report, void *stream);
+
 /* The two halves of tfft_run_protected, for callers that queue several
  * protected transforms before reading their reports (one in-flight protected
  * call per plan): _launch enqueues the fused transform and the tiny

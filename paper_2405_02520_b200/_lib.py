@@ -54,6 +54,9 @@ SIGNATURES = {
                                   ctypes.POINTER(Fault), _INT, ctypes.POINTER(Report), _VP]),
     "tfft_run_protected_host": (_INT, [_VP, _VP, _VP, _I64, _INT, _DBL, _DBL, _VP, _VP,
                                        ctypes.POINTER(Fault), _INT, ctypes.POINTER(Report), _VP]),
+    "tfft_run_campaign": (_INT, [_VP, _VP, _VP, _I64, _I64, _INT, _DBL, _DBL, _VP, _VP,
+                                 ctypes.POINTER(Fault), _INT, ctypes.POINTER(ctypes.c_double),
+                                 ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(Report), _VP]),
     "tfft_protect_launch": (_INT, [_VP, _VP, _VP, _I64, _INT, _DBL, _DBL, _VP, _VP,
                                    ctypes.POINTER(Fault), _INT, ctypes.POINTER(Report), _VP]),
     "tfft_protect_finish": (_INT, [_VP, _VP, _VP, _I64, _INT, _DBL, _DBL, _VP, _VP, _INT,

@@ -50,6 +50,8 @@ struct alignas(64) PassArgs {
     T scale;
     long long f_signal, f_unit;
     int f_idx, f_where, f_comp, f_bit;  // f_where: 1 after load, 2 store pre-scale, 3 post-scale
+    const FaultRec* f_table;          // batched campaign: this pass's fault per f_div signals
+    long long f_div;
 };
 
 // K block-wide sums in one barrier round (thread 0 gets the totals). The
@@ -140,10 +142,25 @@ fft_pass_kernel(const __grid_constant__ PassArgs<T> a) {
         __device__ __forceinline__ void sync() const { __syncthreads(); }
     };
 
+    // Tile order. The first pass with ABFT walks tile-position-major (all
+    // signals' tile i, then tile i+1, ...) so concurrent CTAs read the same
+    // e^T W slice: the input-side table (n elements, up to 512 MB) is then
+    // fetched from HBM about once per launch instead of once per signal.
+    constexpr bool POS_MAJOR = KIND == KIND_FIRST && ABFT != ABFT_OFF;
+    auto tile_of = [&](long long tx, long long& bb, long long& ts) {
+        if constexpr (POS_MAJOR) {
+            ts = tx / a.batch;
+            bb = tx - ts * a.batch;
+        } else {
+            bb = tx / a.tiles_per_sig;
+            ts = tx - bb * a.tiles_per_sig;
+        }
+    };
     // async copy of tile `tx` into `buf` as [j][u] rows of stride RS
     auto issue = [&](long long tx, C<T>* buf) {
-        const long long bb = tx / a.tiles_per_sig;
-        const long long v0 = (tx - bb * a.tiles_per_sig) * U;
+        long long bb, ts;
+        tile_of(tx, bb, ts);
+        const long long v0 = ts * U;
         const long long h0 = v0 / a.lo_count, l0 = v0 - h0 * a.lo_count;
         const C<T>* sb = a.in + bb * a.n + h0 * a.in_hi + l0 * a.in_lo;
         if constexpr (KIND == KIND_LAST) {  // U contiguous rows of L: j fastest
@@ -161,8 +178,9 @@ fft_pass_kernel(const __grid_constant__ PassArgs<T> a) {
     // bulk variant: the ISSUERS threads each arrive with their byte count
     auto issue_bulk = [&](long long tx, C<T>* buf, unsigned long long* bar) {
         if (threadIdx.x >= ISSUERS) return;
-        const long long bb = tx / a.tiles_per_sig;
-        const long long v0 = (tx - bb * a.tiles_per_sig) * U;
+        long long bb, ts;
+        tile_of(tx, bb, ts);
+        const long long v0 = ts * U;
         const long long h0 = v0 / a.lo_count, l0 = v0 - h0 * a.lo_count;
         const C<T>* sb = a.in + bb * a.n + h0 * a.in_hi + l0 * a.in_lo;
         fence_proxy_async();
@@ -203,8 +221,8 @@ fft_pass_kernel(const __grid_constant__ PassArgs<T> a) {
     for (long long tix = blockIdx.x; tix < total; tix += gridDim.x, ++it) {
         C<T>* cur = (PF && (it & 1)) ? tile + BUFE : tile;
         const Mem mem{cur, u};
-        const long long b = tix / a.tiles_per_sig;
-        const long long tsig = tix - b * a.tiles_per_sig;
+        long long b, tsig;
+        tile_of(tix, b, tsig);
         const long long u0 = tsig * U;               // first unit of the tile
         const long long uu = u0 + u;
         const long long hi = uu / a.lo_count, lo = uu - hi * a.lo_count;
@@ -212,9 +230,16 @@ fft_pass_kernel(const __grid_constant__ PassArgs<T> a) {
         C<T>* dst = a.out + b * a.n;
         const long long ibase = hi * a.in_hi + lo * a.in_lo;
         const long long obase = hi * a.out_hi + lo * a.out_lo;
-        const bool fsig = a.f_where != 0 && (a.sig_base + b) == a.f_signal && uu == a.f_unit &&
-                          (a.f_idx % TPS) == t;
-        const int fm = a.f_idx / TPS;
+        int fw = a.f_where, fc = a.f_comp, fb = a.f_bit, fi = a.f_idx;
+        long long fs = a.f_signal, fu = a.f_unit;
+        if (a.f_table != nullptr) {  // batched campaign (never on the product path)
+            const long long g = a.sig_base + b, r = g / a.f_div;
+            const FaultRec fr = a.f_table[r];
+            fw = fr.where; fc = fr.comp; fb = fr.bit; fi = fr.idx;
+            fs = r * a.f_div + fr.signal; fu = fr.pos;
+        }
+        const bool fsig = fw != 0 && (a.sig_base + b) == fs && uu == fu && (fi % TPS) == t;
+        const int fm = fi / TPS;
 
         C<T> v[E];
         if constexpr (BULK) {
@@ -268,13 +293,13 @@ fft_pass_kernel(const __grid_constant__ PassArgs<T> a) {
             T s[3] = {cin.x, cin.y, l1};
             block_reduce<3>(s, red, THREADS / 32);
             if (threadIdx.x == 0) {
-                T* p = a.part + tix * 3;
+                T* p = a.part + (b * a.tiles_per_sig + tsig) * 3;
                 p[0] = s[0]; p[1] = s[1]; p[2] = s[2];
             }
         }
-        if (fsig && a.f_where == 1) {
+        if (fsig && fw == 1) {
 #pragma unroll
-            for (int m = 0; m < E; ++m) if (m == fm) flip_component<T>(v[m], a.f_comp, a.f_bit);
+            for (int m = 0; m < E; ++m) if (m == fm) flip_component<T>(v[m], fc, fb);
         }
 
         if (a.inverse) {
@@ -303,18 +328,18 @@ fft_pass_kernel(const __grid_constant__ PassArgs<T> a) {
 #pragma unroll
             for (int m = 0; m < E; ++m) v[m] = swapri<T>(v[m]);
         }
-        if (fsig && a.f_where == 2) {
+        if (fsig && fw == 2) {
 #pragma unroll
-            for (int m = 0; m < E; ++m) if (m == fm) flip_component<T>(v[m], a.f_comp, a.f_bit);
+            for (int m = 0; m < E; ++m) if (m == fm) flip_component<T>(v[m], fc, fb);
         }
         if constexpr (KIND == KIND_LAST) {
             if (a.scale_inv) {
 #pragma unroll
                 for (int m = 0; m < E; ++m) v[m] = cscale<T>(v[m], a.scale);
             }
-            if (fsig && a.f_where == 3) {
+            if (fsig && fw == 3) {
 #pragma unroll
-                for (int m = 0; m < E; ++m) if (m == fm) flip_component<T>(v[m], a.f_comp, a.f_bit);
+                for (int m = 0; m < E; ++m) if (m == fm) flip_component<T>(v[m], fc, fb);
             }
         }
 #pragma unroll
@@ -338,7 +363,7 @@ fft_pass_kernel(const __grid_constant__ PassArgs<T> a) {
             T s[2] = {cout.x, cout.y};
             block_reduce<2>(s, red, THREADS / 32);
             if (threadIdx.x == 0) {
-                T* p = a.part + tix * 2;
+                T* p = a.part + (b * a.tiles_per_sig + tsig) * 2;
                 p[0] = s[0]; p[1] = s[1];
             }
         }
@@ -358,6 +383,7 @@ struct FinalArgs {
     T* flag_rel;
     long long flag_cap;
     typename KeyT<T>::type* max_key;
+    T* rel_out;  // optional per-signal relative discrepancy
 };
 
 template <class T>
@@ -391,6 +417,7 @@ __global__ void __launch_bounds__(256) abft_finalize_kernel(const FinalArgs<T> a
             T rel = cabs<T>(raw) / den;
             if (!isfinite(rel)) rel = T(INFINITY);
             my_max = my_max > rel ? my_max : rel;
+            if (a.rel_out) a.rel_out[b] = rel;
             if (rel > a.delta) {
                 const int slot = atomicAdd(a.flag_count, 1);
                 if (slot < a.flag_cap) {
@@ -437,6 +464,15 @@ struct MultiPlan {
     size_t ws_bytes = 0;
     void* part = nullptr;                              // ABFT partials
     size_t part_bytes = 0;
+    void* ftab = nullptr;                              // campaign fault tables (one per pass)
+    size_t ftab_bytes = 0;
+};
+
+// One fault per run of a batched campaign, in multi-pass launch codes
+// (where 1 input / 2 stage / 3 output; signal run-relative).
+struct HostFault {
+    long long signal, elem;
+    int where, stage, comp, bit;
 };
 
 struct MultiLaunch {
@@ -455,6 +491,9 @@ struct MultiLaunch {
     long long flag_cap;
     unsigned long long* max_key;
     int only_stage;  // -1: whole transform; k: just stage k, in -> out
+    const HostFault* faults;  // batched campaign: nfaults runs of f_div signals
+    long long nfaults, f_div;
+    void* rel_out;            // optional per-signal relative discrepancy (plan dtype)
 };
 
 int multi_plan_init(MultiPlan& mp, long long n, int prec, int nst, const int64_t* dims, int num_sms);

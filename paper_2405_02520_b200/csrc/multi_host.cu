@@ -129,6 +129,41 @@ const PassEntry* pass_entry(int prec, int logl, int kind) {
 
 int kind_of(int k, int nst) { return k == 0 ? KIND_FIRST : (k == nst - 1 ? KIND_LAST : KIND_MID); }
 
+// A fault (where 1 input / 2 stage:`stage` / 3 output, element e in the
+// reference layout of that hook) in pass k's tile coordinates; returns the
+// pass's where code (0: not in this pass).
+int pass_fault(int k, int nst, long long d0, long long d1, long long d2, long long R0, int where, int stage,
+               long long e, long long& unit, int& idx) {
+    const int kind = kind_of(k, nst);
+    if (where == 1 && k == 0) {                 // input: x[j*R0 + c]
+        unit = e % R0; idx = (int)(e / R0);
+        return 1;
+    }
+    if (where == 2 && stage == k) {             // stage:k, reference layout
+        if (k == 0) {                           // c*d0 + k0
+            unit = e / d0; idx = (int)(e % d0);
+        } else if (kind == KIND_MID) {          // (k0*d2 + c2)*d1 + k1
+            unit = e / d1; idx = (int)(e % d1);
+        } else if (nst == 2) {                  // k0*d1 + k1
+            unit = e / d1; idx = (int)(e % d1);
+        } else {                                // (k0*d1 + k1)*d2 + k2
+            const long long k0 = e / (d1 * d2), k1 = (e / d2) % d1;
+            unit = k1 * d0 + k0; idx = (int)(e % d2);
+        }
+        return 2;
+    }
+    if (where == 3 && kind == KIND_LAST) {      // natural output index f
+        if (nst == 2) {
+            unit = e % d0; idx = (int)(e / d0);
+        } else {
+            const long long k0 = e % d0, k1 = (e / d0) % d1;
+            unit = k1 * d0 + k0; idx = (int)(e / (d0 * d1));
+        }
+        return 3;
+    }
+    return 0;
+}
+
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -252,6 +287,35 @@ int multi_launch_t(MultiPlan& mp, const MultiLaunch& m, cudaStream_t st) {
         part_out = part_in + (size_t)m.batch * tiles[0] * 3;
     }
 
+    if (m.faults && m.nfaults > 0) {  // batched campaign: one fault table per pass
+        std::vector<FaultRec> tab((size_t)nst * m.nfaults);
+        for (int k = 0; k < nst; ++k) {
+            for (long long r = 0; r < m.nfaults; ++r) {
+                const HostFault& f = m.faults[r];
+                FaultRec& fr = tab[(size_t)k * m.nfaults + r];
+                memset(&fr, 0, sizeof(fr));
+                if (f.where == 0) continue;
+                long long unit = 0;
+                int idx = 0;
+                fr.where = pass_fault(k, nst, d0, d1, d2, R0, f.where, f.stage, f.elem, unit, idx);
+                fr.pos = unit;
+                fr.idx = idx;
+                fr.signal = (int)f.signal;
+                fr.comp = f.comp;
+                fr.bit = f.bit;
+            }
+        }
+        const size_t bytes = tab.size() * sizeof(FaultRec);
+        if (bytes > mp.ftab_bytes) {
+            cudaFree(mp.ftab);
+            mp.ftab = nullptr;
+            mp.ftab_bytes = 0;
+            MCU(cudaMalloc(&mp.ftab, bytes));
+            mp.ftab_bytes = bytes;
+        }
+        MCU(cudaMemcpyAsync(mp.ftab, tab.data(), bytes, cudaMemcpyHostToDevice, st));
+        MCU(cudaStreamSynchronize(st));
+    }
     for (int k = 0; k < nst; ++k) {
         if (m.only_stage >= 0 && k != m.only_stage) continue;
         const int kind = k == 0 ? KIND_FIRST : (k == nst - 1 ? KIND_LAST : KIND_MID);
@@ -300,33 +364,18 @@ int multi_launch_t(MultiPlan& mp, const MultiLaunch& m, cudaStream_t st) {
         }
         // fault for this pass
         if (m.f_where != 0) {
-            const long long e = m.f_elem;
             a.f_signal = m.f_signal;
             a.f_comp = m.f_comp;
             a.f_bit = m.f_bit;
-            if (m.f_where == 1 && k == 0) {                 // input: x[j*R0 + c]
-                a.f_where = 1; a.f_unit = e % R0; a.f_idx = (int)(e / R0);
-            } else if (m.f_where == 2 && m.f_stage == k) {  // stage:k, reference layout
-                a.f_where = 2;
-                if (k == 0) {                                // c*d0 + k0
-                    a.f_unit = e / d0; a.f_idx = (int)(e % d0);
-                } else if (kind == KIND_MID) {               // (k0*d2 + c2)*d1 + k1
-                    a.f_unit = e / d1; a.f_idx = (int)(e % d1);
-                } else if (nst == 2) {                       // k0*d1 + k1
-                    a.f_unit = e / d1; a.f_idx = (int)(e % d1);
-                } else {                                     // (k0*d1 + k1)*d2 + k2
-                    const long long k0 = e / (d1 * d2), k1 = (e / d2) % d1;
-                    a.f_unit = k1 * d0 + k0; a.f_idx = (int)(e % d2);
-                }
-            } else if (m.f_where == 3 && kind == KIND_LAST) {  // natural output index f
-                a.f_where = 3;
-                if (nst == 2) {
-                    a.f_unit = e % d0; a.f_idx = (int)(e / d0);
-                } else {
-                    const long long k0 = e % d0, k1 = (e / d0) % d1;
-                    a.f_unit = k1 * d0 + k0; a.f_idx = (int)(e / (d0 * d1));
-                }
-            }
+            long long unit = 0;
+            int idx = 0;
+            a.f_where = pass_fault(k, nst, d0, d1, d2, R0, m.f_where, m.f_stage, m.f_elem, unit, idx);
+            a.f_unit = unit;
+            a.f_idx = idx;
+        }
+        if (m.faults && m.nfaults > 0) {
+            a.f_table = (const FaultRec*)mp.ftab + (size_t)k * m.nfaults;
+            a.f_div = m.f_div;
         }
         if (pe[k]->pf == 3 && kind != KIND_LAST) {
             int rc = encode_rows_tmap<T>(&a.tmap, a.in, kind, n, m.batch, d0, d1, d2, pe[k]->u, mp.d[k]);
@@ -352,6 +401,7 @@ int multi_launch_t(MultiPlan& mp, const MultiLaunch& m, cudaStream_t st) {
         f.flag_rel = (T*)m.flag_rel;
         f.flag_cap = m.flag_cap;
         f.max_key = (typename KeyT<T>::type*)m.max_key;
+        f.rel_out = (T*)m.rel_out;
         const long long grid = std::min<long long>((m.batch + 7) / 8, 4LL * mp.num_sms);
         abft_finalize_kernel<T><<<(unsigned)std::max<long long>(grid, 1), 256, 0, st>>>(f);
         MCU(cudaGetLastError());
@@ -415,6 +465,7 @@ void multi_plan_free(MultiPlan& mp) {
     }
     cudaFree(mp.ws); mp.ws = nullptr; mp.ws_bytes = 0;
     cudaFree(mp.part); mp.part = nullptr; mp.part_bytes = 0;
+    cudaFree(mp.ftab); mp.ftab = nullptr; mp.ftab_bytes = 0;
 }
 
 int multi_launch_stage(MultiPlan& mp, int k, const void* in, void* out, long long batch, int inverse,

@@ -24,6 +24,15 @@ template <class T> struct KeyT;
 template <> struct KeyT<float>  { using type = unsigned int; };
 template <> struct KeyT<double> { using type = unsigned long long; };
 
+// One fault per run of a batched fault campaign (f_table[r] applies to the
+// f_div signals of run r; signal is run-relative). pos: element (single
+// kernel) or tile unit (multi-pass), idx: element within the unit; where uses
+// the launch codes of the kernel (AT_NONE = no fault in this run / pass).
+struct FaultRec {
+    long long pos;
+    int idx, signal, where, comp, bit, pad;
+};
+
 template <class T>
 struct SingleArgs {
     const C<T>* in;
@@ -46,6 +55,8 @@ struct SingleArgs {
     // one device-side fault (reference fault_lab/bits.py:56-77 semantics)
     long long f_signal, f_elem;
     int f_where, f_comp, f_bit;
+    const FaultRec* f_table;  // batched campaign: one fault per f_div signals (overrides f_*)
+    long long f_div;
 };
 
 template <class T> __device__ __forceinline__ T nanmax(T a, T b) {
@@ -244,12 +255,19 @@ fft_single_kernel(const SingleArgs<T> a) {
                 l1 = fadd(l1, mag_fast(v[m]));
             }
         }
-        const bool fault_here = a.f_where != AT_NONE && live && (a.sig_base + b) == a.f_signal &&
-                                (int)(a.f_elem % TPS) == t;
-        const int fm = (int)(a.f_elem / TPS);
-        if (fault_here && a.f_where == AT_INPUT) {
+        int fw = a.f_where, fc = a.f_comp, fb = a.f_bit;
+        long long fs = a.f_signal, fe = a.f_elem;
+        if (a.f_table != nullptr && live) {  // batched campaign (never on the product path)
+            const long long g = a.sig_base + b, r = g / a.f_div;
+            const FaultRec fr = a.f_table[r];
+            fw = fr.where; fc = fr.comp; fb = fr.bit;
+            fs = r * a.f_div + fr.signal; fe = fr.pos;
+        }
+        const bool fault_here = fw != AT_NONE && live && (a.sig_base + b) == fs && (int)(fe % TPS) == t;
+        const int fm = (int)(fe / TPS);
+        if (fault_here && fw == AT_INPUT) {
 #pragma unroll
-            for (int m = 0; m < E; ++m) if (m == fm) flip_component<T>(v[m], a.f_comp, a.f_bit);
+            for (int m = 0; m < E; ++m) if (m == fm) flip_component<T>(v[m], fc, fb);
         }
 
         // ---- transform (inverse = swap(FFT(swap(x))) — conjugate symmetry)
@@ -262,18 +280,18 @@ fft_single_kernel(const SingleArgs<T> a) {
 #pragma unroll
             for (int m = 0; m < E; ++m) v[m] = swapri<T>(v[m]);
         }
-        if (fault_here && a.f_where == AT_PRESCALE) {
+        if (fault_here && fw == AT_PRESCALE) {
 #pragma unroll
-            for (int m = 0; m < E; ++m) if (m == fm) flip_component<T>(v[m], a.f_comp, a.f_bit);
+            for (int m = 0; m < E; ++m) if (m == fm) flip_component<T>(v[m], fc, fb);
         }
         if (a.scale_inv) {
             const T s = T(1) / T(N);  // exact power of two
 #pragma unroll
             for (int m = 0; m < E; ++m) v[m] = cscale<T>(v[m], s);
         }
-        if (fault_here && a.f_where == AT_OUTPUT) {
+        if (fault_here && fw == AT_OUTPUT) {
 #pragma unroll
-            for (int m = 0; m < E; ++m) if (m == fm) flip_component<T>(v[m], a.f_comp, a.f_bit);
+            for (int m = 0; m < E; ++m) if (m == fm) flip_component<T>(v[m], fc, fb);
         }
 
         // ---- store + output checksum

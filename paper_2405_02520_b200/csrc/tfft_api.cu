@@ -185,6 +185,10 @@ struct tfft_plan {
     size_t scratch_bytes = 0;
     FixJob* d_jobs = nullptr;
     int64_t jobs_cap = 0;
+    void* d_ftab = nullptr;         // campaign fault table (single kernel)
+    size_t ftab_bytes = 0;
+    void* d_rel = nullptr;          // campaign per-signal rel discrepancies
+    size_t rel_bytes = 0;
     cudaEvent_t ev_done = nullptr;  // detection summary landed in h_cnt
     // host-streaming path (tfft_run_protected_host): a ring of device chunk
     // buffers, copy streams for each direction, per-slot events
@@ -233,6 +237,12 @@ struct Launch {
     // fault translated for this launch
     long long f_signal, f_elem;
     int f_where, f_stage, f_comp, f_bit;
+    // batched campaign: one fault per f_div signals (device table for the
+    // single kernel, host list for multi-pass) and per-signal rel output
+    const FaultRec* f_table;
+    const HostFault* faults;
+    long long nfaults, f_div;
+    void* rel_out;
 };
 
 template <class T>
@@ -262,7 +272,9 @@ int launch_single_t(tfft_plan* p, const Launch& L, cudaStream_t st) {
     a.flag_rel = (T*)p->d_flag_rel;
     a.flag_cap = p->flag_cap;
     a.max_key = (typename KeyT<T>::type*)&p->d_cnt->max_key;
-    a.rel_out = nullptr;
+    a.rel_out = (T*)L.rel_out;
+    a.f_table = L.f_table;
+    a.f_div = L.f_div;
     a.f_signal = L.f_signal;
     a.f_elem = L.f_elem;
     a.f_where = L.f_where;
@@ -284,6 +296,7 @@ int launch_transform(tfft_plan* p, const Launch& L, cudaStream_t st) {
                                     : launch_single_t<double>(p, L, st);
     }
     MultiLaunch m;
+    memset(&m, 0, sizeof(m));
     m.in = L.in; m.out = L.out; m.batch = L.batch; m.sig_base = L.sig_base;
     m.inverse = L.inverse; m.scale_inv = L.scale_inv; m.abft = L.abft;
     m.etw = L.etw; m.values = L.values; m.delta = L.delta; m.abs_floor = L.abs_floor;
@@ -295,6 +308,10 @@ int launch_transform(tfft_plan* p, const Launch& L, cudaStream_t st) {
     m.flag_cap = p->flag_cap;
     m.max_key = &p->d_cnt->max_key;
     m.only_stage = -1;
+    m.faults = L.faults;
+    m.nfaults = L.nfaults;
+    m.f_div = L.f_div;
+    m.rel_out = L.rel_out;
     int rc = multi_launch(p->multi, m, st);
     if (rc) return fail(rc, multi_last_error());
     return TFFT_OK;
@@ -319,6 +336,63 @@ int check_plan(tfft_plan* p) {
     return TFFT_OK;
 }
 
+// One fault in launch coordinates. Single-kernel plans: where is
+// AT_INPUT / AT_PRESCALE / AT_OUTPUT and elem the natural-order element;
+// multi-pass plans: where 1 input / 2 stage / 3 output with the reference
+// layout index (translated per pass by multi_launch). where == AT_NONE: the
+// fault never fires (outside the batch, or a `where` the reference never
+// emits), like the reference's injector.
+struct FaultT {
+    long long signal = 0, elem = 0;
+    int where = AT_NONE, stage = 0, comp = 0, bit = 0;
+};
+
+int translate_fault(const tfft_plan* p, const tfft_fault& f, int64_t batch, FaultT& out) {
+    out = FaultT();
+    if (f.where == TFFT_AT_NONE) return TFFT_OK;
+    const int64_t n = p->n;
+    const int width = p->prec == TFFT_FP32 ? 32 : 64;
+    bool fires = f.signal >= 0 && f.signal < batch && f.element >= 0 && f.element < n;
+    if (f.where == TFFT_AT_STAGE && (f.stage < 0 || f.stage >= p->nstages)) fires = false;
+    if (f.where < TFFT_AT_NONE || f.where > TFFT_AT_OUTPUT) fires = false;
+    if (!fires) return TFFT_OK;
+    if (f.bit < 0 || f.bit >= width) return fail(TFFT_EINVAL, "bit out of range for the precision");
+    if (f.component != 0 && f.component != 1) return fail(TFFT_EINVAL, "component must be re/im");
+    out.signal = f.signal;
+    out.comp = f.component;
+    out.bit = f.bit;
+    out.stage = f.stage;
+    if (p->single) {
+        if (f.where == TFFT_AT_INPUT) {
+            out.where = AT_INPUT;
+            out.elem = f.element;
+        } else if (f.where == TFFT_AT_OUTPUT) {
+            out.where = AT_OUTPUT;
+            out.elem = f.element;
+        } else {
+            if (f.stage != p->nstages - 1)
+                return fail(TFFT_EUNSUPPORTED, "intermediate-stage injection needs a multi-pass size");
+            // last-stage hook index -> natural order
+            const int64_t e = f.element;
+            int64_t g = e;
+            if (p->nstages == 2) {
+                const int64_t d0 = p->dims[0], d1 = p->dims[1];
+                g = (e / d1) + d0 * (e % d1);
+            } else if (p->nstages == 3) {
+                const int64_t d0 = p->dims[0], d1 = p->dims[1], d2 = p->dims[2];
+                const int64_t k0 = e / (d1 * d2), k1 = (e / d2) % d1, k2 = e % d2;
+                g = k0 + d0 * k1 + d0 * d1 * k2;
+            }
+            out.where = AT_PRESCALE;
+            out.elem = g;
+        }
+    } else {
+        out.where = f.where == TFFT_AT_INPUT ? 1 : (f.where == TFFT_AT_STAGE ? 2 : 3);
+        out.elem = f.element;
+    }
+    return TFFT_OK;
+}
+
 // Validation, report reset and the fault translated into launch coordinates
 // (shared by the device and the host-streaming entry points).
 int prepare_protected(tfft_plan* p, const void* in, void* out, int64_t batch, int scheme, double delta,
@@ -332,7 +406,6 @@ int prepare_protected(tfft_plan* p, const void* in, void* out, int64_t batch, in
     if (prot && !etw) return fail(TFFT_EINVAL, "protected schemes need the encoding row");
     if (prot && !(delta > 0)) return fail(TFFT_EINVAL, "delta must be positive");
     const int64_t groups = batch / p->bs;
-    const int64_t n = p->n;
     rep->groups = groups;
     rep->recompute_count = 0;
     rep->pass_count = 2 * (int64_t)p->nstages * groups;
@@ -348,44 +421,16 @@ int prepare_protected(tfft_plan* p, const void* in, void* out, int64_t batch, in
     L.abs_floor = abs_floor;
     // ---- translate the fault into the launch's coordinates
     if (fault && fault->where != TFFT_AT_NONE) {
-        const int width = p->prec == TFFT_FP32 ? 32 : 64;
-        bool fires = fault->signal >= 0 && fault->signal < batch && fault->element >= 0 && fault->element < n;
-        if (fault->where == TFFT_AT_STAGE && (fault->stage < 0 || fault->stage >= p->nstages)) fires = false;
-        if (fires) {
-            if (fault->bit < 0 || fault->bit >= width) return fail(TFFT_EINVAL, "bit out of range for the precision");
-            if (fault->component != 0 && fault->component != 1) return fail(TFFT_EINVAL, "component must be re/im");
-            L.f_signal = fault->signal;
-            L.f_comp = fault->component;
-            L.f_bit = fault->bit;
-            L.f_stage = fault->stage;
-            if (p->single) {
-                if (fault->where == TFFT_AT_INPUT) {
-                    L.f_where = AT_INPUT;
-                    L.f_elem = fault->element;
-                } else if (fault->where == TFFT_AT_OUTPUT) {
-                    L.f_where = AT_OUTPUT;
-                    L.f_elem = fault->element;
-                } else {
-                    if (fault->stage != p->nstages - 1)
-                        return fail(TFFT_EUNSUPPORTED, "intermediate-stage injection needs a multi-pass size");
-                    // last-stage hook index -> natural order
-                    const int64_t e = fault->element;
-                    int64_t f = e;
-                    if (p->nstages == 2) {
-                        const int64_t d0 = p->dims[0], d1 = p->dims[1];
-                        f = (e / d1) + d0 * (e % d1);
-                    } else if (p->nstages == 3) {
-                        const int64_t d0 = p->dims[0], d1 = p->dims[1], d2 = p->dims[2];
-                        const int64_t k0 = e / (d1 * d2), k1 = (e / d2) % d1, k2 = e % d2;
-                        f = k0 + d0 * k1 + d0 * d1 * k2;
-                    }
-                    L.f_where = AT_PRESCALE;
-                    L.f_elem = f;
-                }
-            } else {
-                L.f_where = fault->where == TFFT_AT_INPUT ? 1 : (fault->where == TFFT_AT_STAGE ? 2 : 3);
-                L.f_elem = fault->element;
-            }
+        FaultT ft;
+        int rc = translate_fault(p, *fault, batch, ft);
+        if (rc) return rc;
+        if (ft.where != AT_NONE) {
+            L.f_signal = ft.signal;
+            L.f_elem = ft.elem;
+            L.f_where = ft.where;
+            L.f_stage = ft.stage;
+            L.f_comp = ft.comp;
+            L.f_bit = ft.bit;
             rep->fault_fired = 1;
         }
     }
@@ -491,6 +536,8 @@ int tfft_plan_destroy(tfft_plan* p) {
     cudaFree(p->d_flag_rel);
     cudaFree(p->d_scratch);
     cudaFree(p->d_jobs);
+    cudaFree(p->d_ftab);
+    cudaFree(p->d_rel);
     if (p->ev_done) cudaEventDestroy(p->ev_done);
     cudaFree(p->ring);
     for (int i = 0; i < tfft_plan::kRing; ++i) {
@@ -1022,6 +1069,116 @@ int tfft_run_protected_host(tfft_plan* p, const void* in, void* out, int64_t bat
         fixed_ok[i] = ok1[0];
     }
     fill_lists(p, scheme, rep, bad_groups, fix_groups, fix_sig, fixed_ok);
+    return TFFT_OK;
+}
+
+// Batched fault campaign (reference fault_lab/campaign.py:95-195): `runs`
+// independent protected calls of `run_batch` signals fused into one launch,
+// each run with its own single fault (faults[r], run-relative signal).
+int tfft_run_campaign(tfft_plan* p, const void* in, void* out, int64_t runs, int64_t run_batch, int scheme,
+                      double delta, double abs_floor, const void* etw, const void* values,
+                      const tfft_fault* faults, int inverse, double* run_max_rel, int32_t* run_fired,
+                      tfft_report* rep, void* stream) {
+    int rc = check_plan(p);
+    if (rc) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (runs < 1 || run_batch < 1) return fail(TFFT_EINVAL, "runs and run_batch must be >= 1");
+    if (run_batch % p->bs) return fail(TFFT_EINVAL, "run_batch not divisible by group size");
+    if (scheme == TFFT_SCHEME_NONE) return fail(TFFT_EINVAL, "a campaign needs a protected scheme");
+    if (!run_max_rel) return fail(TFFT_EINVAL, "null run_max_rel");
+    const int64_t batch = runs * run_batch;
+    Launch L;
+    rc = prepare_protected(p, in, out, batch, scheme, delta, etw, values, abs_floor, nullptr, inverse, rep, L);
+    if (rc) return rc;
+    // ---- per-run faults, translated like the single-fault path
+    std::vector<FaultRec> tab;
+    std::vector<HostFault> hf;
+    bool any = false;
+    if (faults) {
+        if (p->single) tab.assign(runs, FaultRec{});
+        else hf.assign(runs, HostFault{});
+        for (int64_t r = 0; r < runs; ++r) {
+            FaultT ft;
+            rc = translate_fault(p, faults[r], run_batch, ft);
+            if (rc) return rc;
+            if (run_fired) run_fired[r] = ft.where != AT_NONE;
+            if (ft.where == AT_NONE) continue;
+            any = true;
+            if (p->single) {
+                tab[r].pos = ft.elem;
+                tab[r].signal = (int)ft.signal;
+                tab[r].where = ft.where;
+                tab[r].comp = ft.comp;
+                tab[r].bit = ft.bit;
+            } else {
+                hf[r].signal = ft.signal;
+                hf[r].elem = ft.elem;
+                hf[r].where = ft.where;
+                hf[r].stage = ft.stage;
+                hf[r].comp = ft.comp;
+                hf[r].bit = ft.bit;
+            }
+        }
+    } else if (run_fired) {
+        for (int64_t r = 0; r < runs; ++r) run_fired[r] = 0;
+    }
+    if (any) {
+        L.f_div = run_batch;
+        if (p->single) {
+            const size_t bytes = tab.size() * sizeof(FaultRec);
+            if (bytes > p->ftab_bytes) {
+                cudaFree(p->d_ftab);
+                p->d_ftab = nullptr;
+                p->ftab_bytes = 0;
+                CU(cudaMalloc(&p->d_ftab, bytes));
+                p->ftab_bytes = bytes;
+            }
+            CU(cudaMemcpyAsync(p->d_ftab, tab.data(), bytes, cudaMemcpyHostToDevice, st));
+            L.f_table = (const FaultRec*)p->d_ftab;
+        } else {
+            L.faults = hf.data();
+            L.nfaults = runs;
+        }
+    }
+    const size_t tb = p->prec == TFFT_FP32 ? 4 : 8;
+    if (batch * tb > p->rel_bytes) {
+        cudaFree(p->d_rel);
+        p->d_rel = nullptr;
+        p->rel_bytes = 0;
+        CU(cudaMalloc(&p->d_rel, batch * tb));
+        p->rel_bytes = batch * tb;
+    }
+    L.rel_out = p->d_rel;
+    rc = ensure_flags(p, batch);
+    if (rc) return rc;
+    CU(cudaMemsetAsync(p->d_cnt, 0, sizeof(Counters), st));
+    rc = launch_transform(p, L, st);
+    if (rc) return rc;
+    CU(cudaMemcpyAsync(p->h_cnt, p->d_cnt, sizeof(Counters), cudaMemcpyDeviceToHost, st));
+    if (!p->ev_done) CU(cudaEventCreateWithFlags(&p->ev_done, cudaEventDisableTiming));
+    CU(cudaEventRecord(p->ev_done, st));
+    // per-run max discrepancy (protected.py:124-126 max over the run's groups)
+    std::vector<char> rel((size_t)batch * tb);
+    CU(cudaMemcpyAsync(rel.data(), p->d_rel, batch * tb, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    for (int64_t r = 0; r < runs; ++r) {
+        double mx = 0.0;
+        for (int64_t i = r * run_batch; i < (r + 1) * run_batch; ++i) {
+            const double v = tb == 4 ? (double)((const float*)rel.data())[i] : ((const double*)rel.data())[i];
+            if (v > mx || v != v) mx = v != v ? INFINITY : v;
+        }
+        run_max_rel[r] = mx;
+    }
+    std::vector<std::pair<long long, double>> flags;
+    rc = read_summary(p, batch, st, rep, flags);
+    if (rc) return rc;
+    std::vector<int64_t> bad_groups, fix_groups, fix_sig;
+    decide(p, flags, bad_groups, fix_groups, fix_sig);
+    std::vector<char> fixed_ok;
+    rc = correct_groups(p, in, out, scheme, etw, values, delta, abs_floor, inverse, fix_groups, fix_sig, fixed_ok, st);
+    if (rc) return rc;
+    fill_lists(p, scheme, rep, bad_groups, fix_groups, fix_sig, fixed_ok);
+    rep->fault_fired = any;
     return TFFT_OK;
 }
 

@@ -1,12 +1,19 @@
-# ncu --set full captures of single kernels, ABFT on vs off (usage: bash tools/gpu_prof.sh TAG "prec:logn ..." )
+# ncu --set full captures, ABFT on vs off, summarised on the box (reports over
+# 20 MB are deleted after summarising so gpurun_out stays under its cap).
+# usage: KRE=<kernel regex> COUNT=<kernels per capture> bash tools/gpu_prof.sh TAG prec:logn ...
 set -x
 cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
 TAG=$1; shift
 for spec in $@; do
   p=${spec%%:*}; l=${spec##*:}
   for sc in two_sided_group none; do
-    timeout 600 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:"${KRE:-fft_single_kernel<float}" -s 1 -c 1 \
-      -o gpurun_out/${TAG}_${p}_n${l}_${sc} -f python tools/profile_single.py --prec $p --logn $l --scheme $sc --reps 2 > gpurun_out/${TAG}_${p}_n${l}_${sc}.log 2>&1
+    o=gpurun_out/${TAG}_${p}_n${l}_${sc}
+    timeout 900 ncu --set full --clock-control none --import-source on --profile-from-start off \
+      --kernel-name-base demangled -k regex:"${KRE:-fft_}" -c ${COUNT:-1} \
+      -o $o -f python tools/profile_single.py --prec $p --logn $l --scheme $sc --reps 2 > $o.log 2>&1
+    python tools/ncu_summary.py $o.ncu-rep > $o.md 2>&1
+    python tools/sass_hot.py $o.ncu-rep --top 30 --lines 40 > $o.sass.txt 2>&1
+    if [ $(stat -c %s $o.ncu-rep) -gt 20000000 ]; then rm -f $o.ncu-rep; fi
   done
 done
-ls -la gpurun_out
+du -sh gpurun_out
