@@ -26,7 +26,8 @@ enum tfft_status {
     TFFT_EINVAL = 1,        /* bad argument      -> Python ValueError   */
     TFFT_ECUDA = 3,         /* CUDA failure      -> Python RuntimeError */
     TFFT_ENOMEM = 4,        /* allocation failed -> Python MemoryError  */
-    TFFT_EUNSUPPORTED = 5   /* size/precision not built                 */
+    TFFT_EUNSUPPORTED = 5,  /* size/precision not built                 */
+    TFFT_EIO = 6            /* file I/O failure  -> Python OSError      */
 };
 
 enum tfft_precision { TFFT_FP32 = 0, TFFT_FP64 = 1 };
@@ -118,6 +119,24 @@ int tfft_run_protected_host(tfft_plan *plan, const void *in, void *out, int64_t 
                             const void *etw, const void *values,
                             const tfft_fault *fault, int inverse,
                             tfft_report *report, void *stream);
+
+/* signal_io.py:11-24 read_signals size check: number of n-sample signals of
+ * the precision in a raw interleaved (re, im) little-endian file, or
+ * TFFT_EINVAL ("input length mismatch ...") when the size is not a positive
+ * whole number of signals. */
+int tfft_signal_file_batch(const char *path, int64_t n, int precision, int64_t *batch);
+
+/* cli.py:54-67 cmd_transform over files (signal_io.py:11-33 formats): reads
+ * the raw input file, runs the protected transform and writes the raw output
+ * file (created/truncated), streaming chunks of whole groups through pinned
+ * staging with file reads, H2D, the fused transform, D2H and file writes of
+ * different chunks overlapped (a writer thread retires chunks in order).
+ * *batch receives the signal count. The output is written even when groups
+ * are unrecoverable (the report says so); I/O errors return TFFT_EIO. */
+int tfft_run_protected_file(tfft_plan *plan, const char *in_path, const char *out_path,
+                            int scheme, double delta, double abs_floor,
+                            const void *etw, const void *values, const tfft_fault *fault,
+                            int inverse, int64_t *batch, tfft_report *report, void *stream);
 
 /* Batched fault-injection campaign (fault_lab/campaign.py:95-195, the run
  * loop of run_campaign): `runs` independent run_protected calls of

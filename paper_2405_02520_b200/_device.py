@@ -79,6 +79,10 @@ def to_host(t: torch.Tensor) -> np.ndarray:
     return h.numpy()
 
 
+def torch_current_device() -> int:
+    return torch.cuda.current_device()
+
+
 def stream_ptr():
     return torch.cuda.current_stream().cuda_stream
 

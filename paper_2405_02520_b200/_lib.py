@@ -13,7 +13,7 @@ import threading
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libtfft.so")
 
-TFFT_OK, TFFT_EINVAL, TFFT_ECUDA, TFFT_ENOMEM, TFFT_EUNSUPPORTED = 0, 1, 3, 4, 5
+TFFT_OK, TFFT_EINVAL, TFFT_ECUDA, TFFT_ENOMEM, TFFT_EUNSUPPORTED, TFFT_EIO = 0, 1, 3, 4, 5, 6
 FP32, FP64 = 0, 1
 AT_NONE, AT_INPUT, AT_STAGE, AT_OUTPUT = 0, 1, 2, 3
 SCHEME_CODE = {"none": 0, "one_sided": 1, "two_sided_thread": 2, "two_sided_group": 3}
@@ -54,6 +54,10 @@ SIGNATURES = {
                                   ctypes.POINTER(Fault), _INT, ctypes.POINTER(Report), _VP]),
     "tfft_run_protected_host": (_INT, [_VP, _VP, _VP, _I64, _INT, _DBL, _DBL, _VP, _VP,
                                        ctypes.POINTER(Fault), _INT, ctypes.POINTER(Report), _VP]),
+    "tfft_signal_file_batch": (_INT, [ctypes.c_char_p, _I64, _INT, ctypes.POINTER(_I64)]),
+    "tfft_run_protected_file": (_INT, [_VP, ctypes.c_char_p, ctypes.c_char_p, _INT, _DBL, _DBL, _VP, _VP,
+                                       ctypes.POINTER(Fault), _INT, ctypes.POINTER(_I64),
+                                       ctypes.POINTER(Report), _VP]),
     "tfft_run_campaign": (_INT, [_VP, _VP, _VP, _I64, _I64, _INT, _DBL, _DBL, _VP, _VP,
                                  ctypes.POINTER(Fault), _INT, ctypes.POINTER(ctypes.c_double),
                                  ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(Report), _VP]),
@@ -115,4 +119,6 @@ def check(rc: int, what: str = ""):
         raise MemoryError(text)
     if rc == TFFT_EUNSUPPORTED:
         raise NotImplementedError(text)
+    if rc == TFFT_EIO:
+        raise OSError(text)
     raise TfftError(text)

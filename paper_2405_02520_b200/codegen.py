@@ -288,8 +288,8 @@ PASS_CANDIDATES = {
 # (first, middle, last) variant per log2 L; missing -> (0, 0, 0).
 # Source: tools/tune_pass.py on a B200, ABFT on, 1 GiB (profiles/tune_pass_r01.json).
 PASS_CHOICE = {
-    "fp32": {7: (6, 6, 5), 8: (6, 6, 7), 9: (6, 0, 7), 10: (7, 0, 6), 11: (6, 0, 6)},
-    "fp64": {7: (6, 6, 6), 8: (7, 6, 6), 9: (6, 0, 7), 10: (0, 0, 4), 11: (0, 0, 3)},
+    "fp32": {7: (6, 6, 5), 8: (6, 6, 5), 9: (6, 0, 7), 10: (7, 0, 8), 11: (6, 0, 6)},
+    "fp64": {7: (3, 6, 4), 8: (7, 6, 4), 9: (7, 0, 5), 10: (6, 0, 6), 11: (0, 0, 3)},
 }
 
 

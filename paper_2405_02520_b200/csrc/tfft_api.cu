@@ -2,14 +2,21 @@
 // launch dispatch and the run_protected orchestration
 // (reference abft/protected.py:63-166).
 #include <cuda_runtime.h>
+#include <fcntl.h>
+#include <sys/stat.h>
+#include <unistd.h>
 
 #include <algorithm>
+#include <atomic>
+#include <cerrno>
 #include <cmath>
+#include <condition_variable>
 #include <cstdio>
 #include <cstring>
 #include <map>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/tfft.h"
@@ -197,6 +204,8 @@ struct tfft_plan {
     void* ring = nullptr;           // kRing x (in chunk, out chunk)
     size_t ring_chunk = 0;          // bytes of one chunk buffer
     cudaEvent_t ev_in[kRing] = {}, ev_comp[kRing] = {}, ev_out[kRing] = {};
+    void* h_stage = nullptr;        // file path: pinned kRing x (in chunk, out chunk)
+    size_t h_stage_chunk = 0;
 };
 
 namespace {
@@ -393,6 +402,42 @@ int translate_fault(const tfft_plan* p, const tfft_fault& f, int64_t batch, Faul
     return TFFT_OK;
 }
 
+// Copy streams, per-slot events and the device chunk ring of the streaming
+// (host / file) paths.
+int ensure_ring(tfft_plan* p, size_t chunk, cudaStream_t st) {
+    if (!p->s_h2d) {
+        CU(cudaStreamCreateWithFlags(&p->s_h2d, cudaStreamNonBlocking));
+        CU(cudaStreamCreateWithFlags(&p->s_d2h, cudaStreamNonBlocking));
+        for (int i = 0; i < tfft_plan::kRing; ++i) {
+            CU(cudaEventCreateWithFlags(&p->ev_in[i], cudaEventDisableTiming));
+            CU(cudaEventCreateWithFlags(&p->ev_comp[i], cudaEventDisableTiming));
+            CU(cudaEventCreateWithFlags(&p->ev_out[i], cudaEventDisableTiming));
+        }
+    }
+    if (!p->ev_done) CU(cudaEventCreateWithFlags(&p->ev_done, cudaEventDisableTiming));
+    if (chunk > p->ring_chunk) {
+        CU(cudaStreamSynchronize(st));
+        CU(cudaStreamSynchronize(p->s_h2d));
+        CU(cudaStreamSynchronize(p->s_d2h));
+        cudaFree(p->ring);
+        p->ring = nullptr;
+        p->ring_chunk = 0;
+        if (cudaMalloc(&p->ring, 2 * tfft_plan::kRing * chunk) != cudaSuccess)
+            return fail(TFFT_ENOMEM, "host-streaming ring");
+        p->ring_chunk = chunk;
+    }
+    return TFFT_OK;
+}
+
+// Whole checksum groups per streaming chunk: ~32 MiB, deep enough to hide
+// launch gaps, small enough that pipeline fill/drain is a few percent of a
+// 1 GiB batch.
+int64_t groups_per_chunk(const tfft_plan* p, int64_t batch) {
+    const int64_t grp_bytes = p->n * (int64_t)p->esize * p->bs;
+    int64_t gpc = std::max<int64_t>(1, ((int64_t)1 << 25) / grp_bytes);
+    return std::min<int64_t>(gpc, batch / p->bs);
+}
+
 // Validation, report reset and the fault translated into launch coordinates
 // (shared by the device and the host-streaming entry points).
 int prepare_protected(tfft_plan* p, const void* in, void* out, int64_t batch, int scheme, double delta,
@@ -540,6 +585,7 @@ int tfft_plan_destroy(tfft_plan* p) {
     cudaFree(p->d_rel);
     if (p->ev_done) cudaEventDestroy(p->ev_done);
     cudaFree(p->ring);
+    if (p->h_stage) cudaFreeHost(p->h_stage);
     for (int i = 0; i < tfft_plan::kRing; ++i) {
         if (p->ev_in[i]) cudaEventDestroy(p->ev_in[i]);
         if (p->ev_comp[i]) cudaEventDestroy(p->ev_comp[i]);
@@ -974,33 +1020,10 @@ int tfft_run_protected_host(tfft_plan* p, const void* in, void* out, int64_t bat
     const bool prot = scheme != TFFT_SCHEME_NONE;
     const size_t sig_bytes = (size_t)p->n * p->esize;
     const size_t grp_bytes = sig_bytes * p->bs;
-    // ~32 MiB chunks (whole groups): deep enough to hide launch gaps, small
-    // enough that the pipeline fill/drain is a few percent of a 1 GiB batch
-    const int64_t target = (int64_t)1 << 25;
-    int64_t gpc = std::max<int64_t>(1, target / (int64_t)grp_bytes);
-    gpc = std::min<int64_t>(gpc, batch / p->bs);
+    const int64_t gpc = groups_per_chunk(p, batch);
     const size_t chunk = (size_t)gpc * grp_bytes;
-    if (!p->s_h2d) {
-        CU(cudaStreamCreateWithFlags(&p->s_h2d, cudaStreamNonBlocking));
-        CU(cudaStreamCreateWithFlags(&p->s_d2h, cudaStreamNonBlocking));
-        for (int i = 0; i < tfft_plan::kRing; ++i) {
-            CU(cudaEventCreateWithFlags(&p->ev_in[i], cudaEventDisableTiming));
-            CU(cudaEventCreateWithFlags(&p->ev_comp[i], cudaEventDisableTiming));
-            CU(cudaEventCreateWithFlags(&p->ev_out[i], cudaEventDisableTiming));
-        }
-    }
-    if (!p->ev_done) CU(cudaEventCreateWithFlags(&p->ev_done, cudaEventDisableTiming));
-    if (chunk > p->ring_chunk) {
-        CU(cudaStreamSynchronize(st));
-        CU(cudaStreamSynchronize(p->s_h2d));
-        CU(cudaStreamSynchronize(p->s_d2h));
-        cudaFree(p->ring);
-        p->ring = nullptr;
-        p->ring_chunk = 0;
-        if (cudaMalloc(&p->ring, 2 * tfft_plan::kRing * chunk) != cudaSuccess)
-            return fail(TFFT_ENOMEM, "host-streaming ring");
-        p->ring_chunk = chunk;
-    }
+    rc = ensure_ring(p, chunk, st);
+    if (rc) return rc;
     if (prot) {
         rc = ensure_flags(p, batch);
         if (rc) return rc;
@@ -1179,6 +1202,239 @@ int tfft_run_campaign(tfft_plan* p, const void* in, void* out, int64_t runs, int
     if (rc) return rc;
     fill_lists(p, scheme, rep, bad_groups, fix_groups, fix_sig, fixed_ok);
     rep->fault_fired = any;
+    return TFFT_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+struct Fd {
+    int fd = -1;
+    ~Fd() { if (fd >= 0) close(fd); }
+};
+
+int io_fail(const char* what, const char* path) {
+    return fail(TFFT_EIO, std::string(what) + " " + path + ": " + strerror(errno));
+}
+
+// full-length pread / pwrite (short transfers retried)
+bool read_at(int fd, void* buf, size_t bytes, off_t off) {
+    char* b = (char*)buf;
+    while (bytes) {
+        const ssize_t r = pread(fd, b, bytes, off);
+        if (r < 0 && errno == EINTR) continue;
+        if (r <= 0) return false;
+        b += r; off += r; bytes -= (size_t)r;
+    }
+    return true;
+}
+bool write_at(int fd, const void* buf, size_t bytes, off_t off) {
+    const char* b = (const char*)buf;
+    while (bytes) {
+        const ssize_t r = pwrite(fd, b, bytes, off);
+        if (r < 0 && errno == EINTR) continue;
+        if (r <= 0) return false;
+        b += r; off += r; bytes -= (size_t)r;
+    }
+    return true;
+}
+
+}  // namespace
+
+extern "C" {
+
+int tfft_signal_file_batch(const char* path, int64_t n, int precision, int64_t* batch) {
+    if (!path || !batch) return fail(TFFT_EINVAL, "null argument");
+    if (precision != TFFT_FP32 && precision != TFFT_FP64) return fail(TFFT_EINVAL, "bad precision");
+    struct stat sb;
+    if (stat(path, &sb) != 0) return io_fail("cannot stat", path);
+    const int64_t sig = n * (precision == TFFT_FP32 ? 8 : 16);
+    if (sb.st_size == 0 || sb.st_size % sig) {
+        return fail(TFFT_EINVAL, "input length mismatch: " + std::to_string((long long)sb.st_size) +
+                                     " bytes is not a whole number of " + std::to_string((long long)n) +
+                                     "-sample " + (precision == TFFT_FP32 ? "fp32" : "fp64") + " signals");
+    }
+    *batch = sb.st_size / sig;
+    return TFFT_OK;
+}
+
+// cli.py:54-67 cmd_transform + signal_io.py:11-33: raw interleaved (re, im)
+// little-endian files are the complex64 / complex128 memory layout, so the
+// file is streamed chunk by chunk: pread into a pinned slot -> H2D -> fused
+// protected transform -> D2H into a pinned slot -> pwrite by a writer thread,
+// all stages of different chunks in flight at once.
+int tfft_run_protected_file(tfft_plan* p, const char* in_path, const char* out_path, int scheme, double delta,
+                            double abs_floor, const void* etw, const void* values, const tfft_fault* fault,
+                            int inverse, int64_t* batch_out, tfft_report* rep, void* stream) {
+    int rc = check_plan(p);
+    if (rc) return rc;
+    if (!in_path || !out_path) return fail(TFFT_EINVAL, "null path");
+    cudaStream_t st = (cudaStream_t)stream;
+    int64_t batch = 0;
+    rc = tfft_signal_file_batch(in_path, p->n, p->prec, &batch);
+    if (rc) return rc;
+    if (batch_out) *batch_out = batch;
+    Launch L;
+    static char dummy;
+    rc = prepare_protected(p, &dummy, &dummy, batch, scheme, delta, etw, values, abs_floor, fault, inverse, rep, L);
+    if (rc) return rc;
+    const bool prot = scheme != TFFT_SCHEME_NONE;
+    Fd fin, fout;
+    fin.fd = open(in_path, O_RDONLY);
+    if (fin.fd < 0) return io_fail("cannot open", in_path);
+    fout.fd = open(out_path, O_WRONLY | O_CREAT | O_TRUNC, 0644);
+    if (fout.fd < 0) return io_fail("cannot create", out_path);
+    const size_t sig_bytes = (size_t)p->n * p->esize;
+    const size_t grp_bytes = sig_bytes * p->bs;
+    if (ftruncate(fout.fd, (off_t)(batch * sig_bytes)) != 0) return io_fail("cannot size", out_path);
+    const int64_t gpc = groups_per_chunk(p, batch);
+    const size_t chunk = (size_t)gpc * grp_bytes;
+    rc = ensure_ring(p, chunk, st);
+    if (rc) return rc;
+    constexpr int R = tfft_plan::kRing;
+    if (chunk > p->h_stage_chunk) {
+        if (p->h_stage) cudaFreeHost(p->h_stage);
+        p->h_stage = nullptr;
+        p->h_stage_chunk = 0;
+        if (cudaHostAlloc(&p->h_stage, 2 * R * chunk, cudaHostAllocDefault) != cudaSuccess)
+            return fail(TFFT_ENOMEM, "pinned file staging");
+        p->h_stage_chunk = chunk;
+    }
+    auto hin = [&](int slot) { return (char*)p->h_stage + (size_t)slot * 2 * p->h_stage_chunk; };
+    auto hout = [&](int slot) { return hin(slot) + p->h_stage_chunk; };
+    if (prot) {
+        rc = ensure_flags(p, batch);
+        if (rc) return rc;
+        CU(cudaMemsetAsync(p->d_cnt, 0, sizeof(Counters), st));
+    }
+    CU(cudaEventRecord(p->ev_done, st));
+    CU(cudaStreamWaitEvent(p->s_h2d, p->ev_done, 0));
+    CU(cudaStreamWaitEvent(p->s_d2h, p->ev_done, 0));
+    const int64_t spc = gpc * p->bs;
+    const int64_t nchunks = (batch + spc - 1) / spc;
+
+    // writer: retires chunks in order (waits for their D2H, pwrites them)
+    std::mutex mu;
+    std::condition_variable cv;
+    int64_t queued = 0, written = 0;  // chunks handed to / finished by the writer
+    std::atomic<int> werr{0};
+    std::string werr_msg;
+    std::thread writer([&] {
+        for (int64_t c = 0; c < nchunks; ++c) {
+            {
+                std::unique_lock<std::mutex> lk(mu);
+                cv.wait(lk, [&] { return queued > c || werr.load(); });
+            }
+            if (werr.load()) break;
+            const int slot = (int)(c % R);
+            const int64_t s0 = c * spc;
+            const size_t bytes = (size_t)std::min<int64_t>(spc, batch - s0) * sig_bytes;
+            if (cudaEventSynchronize(p->ev_out[slot]) != cudaSuccess) {
+                werr_msg = "D2H failed";
+                werr = TFFT_ECUDA;
+            } else if (!write_at(fout.fd, hout(slot), bytes, (off_t)(s0 * sig_bytes))) {
+                werr_msg = std::string("cannot write ") + out_path + ": " + strerror(errno);
+                werr = TFFT_EIO;
+            }
+            {
+                std::lock_guard<std::mutex> lk(mu);
+                written = c + 1;
+            }
+            cv.notify_all();
+            if (werr.load()) break;
+        }
+    });
+    auto stop_writer = [&](int code, const std::string& msg) {
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            if (!werr.load()) {
+                werr = code ? code : TFFT_ECUDA;
+                werr_msg = msg;
+            }
+        }
+        cv.notify_all();
+        writer.join();
+        return fail(werr.load(), werr_msg);
+    };
+    for (int64_t c = 0; c < nchunks; ++c) {
+        const int slot = (int)(c % R);
+        char* din = (char*)p->ring + (size_t)slot * 2 * p->ring_chunk;
+        char* dout = din + p->ring_chunk;
+        const int64_t s0 = c * spc;
+        const int64_t ns = std::min<int64_t>(spc, batch - s0);
+        const size_t bytes = (size_t)ns * sig_bytes;
+        {  // slot free: the writer has retired chunk c - R
+            std::unique_lock<std::mutex> lk(mu);
+            cv.wait(lk, [&] { return written >= c - R + 1 || werr.load(); });
+        }
+        if (werr.load()) {
+            writer.join();
+            return fail(werr.load(), werr_msg);
+        }
+        if (!read_at(fin.fd, hin(slot), bytes, (off_t)(s0 * sig_bytes)))
+            return stop_writer(TFFT_EIO, std::string("cannot read ") + in_path + ": " + strerror(errno));
+        if (cudaMemcpyAsync(din, hin(slot), bytes, cudaMemcpyHostToDevice, p->s_h2d) != cudaSuccess ||
+            cudaEventRecord(p->ev_in[slot], p->s_h2d) != cudaSuccess ||
+            cudaStreamWaitEvent(st, p->ev_in[slot], 0) != cudaSuccess)
+            return stop_writer(TFFT_ECUDA, "H2D enqueue failed");
+        Launch C = L;
+        C.in = din;
+        C.out = dout;
+        C.batch = ns;
+        C.sig_base = s0;
+        rc = launch_transform(p, C, st);
+        if (rc) return stop_writer(rc, g_err);
+        if (cudaEventRecord(p->ev_comp[slot], st) != cudaSuccess ||
+            cudaStreamWaitEvent(p->s_d2h, p->ev_comp[slot], 0) != cudaSuccess ||
+            cudaMemcpyAsync(hout(slot), dout, bytes, cudaMemcpyDeviceToHost, p->s_d2h) != cudaSuccess ||
+            cudaEventRecord(p->ev_out[slot], p->s_d2h) != cudaSuccess)
+            return stop_writer(TFFT_ECUDA, "D2H enqueue failed");
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            queued = c + 1;
+        }
+        cv.notify_all();
+    }
+    writer.join();
+    if (werr.load()) return fail(werr.load(), werr_msg);
+    CU(cudaStreamSynchronize(p->s_d2h));
+    if (!prot) return TFFT_OK;
+    CU(cudaMemcpyAsync(p->h_cnt, p->d_cnt, sizeof(Counters), cudaMemcpyDeviceToHost, st));
+    CU(cudaEventRecord(p->ev_done, st));
+    std::vector<std::pair<long long, double>> flags;
+    rc = read_summary(p, batch, st, rep, flags);
+    if (rc) return rc;
+    std::vector<int64_t> bad_groups, fix_groups, fix_sig;
+    decide(p, flags, bad_groups, fix_groups, fix_sig);
+    std::vector<char> fixed_ok(fix_groups.size(), 0);
+    // rare path: each candidate group's clean input and current output are
+    // re-staged from the files, corrected on the device and written back
+    char* din = (char*)p->ring;
+    char* dout = din + p->ring_chunk;
+    int infd2 = open(out_path, O_RDONLY);
+    if (!fix_groups.empty() && infd2 < 0) return io_fail("cannot reopen", out_path);
+    Fd fo2;
+    fo2.fd = infd2;
+    for (size_t i = 0; i < fix_groups.size(); ++i) {
+        const int64_t g = fix_groups[i];
+        const off_t off = (off_t)(g * grp_bytes);
+        if (!read_at(fin.fd, hin(0), grp_bytes, off)) return io_fail("cannot read", in_path);
+        if (!read_at(fo2.fd, hout(0), grp_bytes, off)) return io_fail("cannot read", out_path);
+        CU(cudaMemcpyAsync(din, hin(0), grp_bytes, cudaMemcpyHostToDevice, st));
+        CU(cudaMemcpyAsync(dout, hout(0), grp_bytes, cudaMemcpyHostToDevice, st));
+        std::vector<int64_t> g1{0}, s1{fix_sig[i] - g * p->bs};
+        std::vector<char> ok1;
+        rc = correct_groups(p, din, dout, scheme, etw, values, delta, abs_floor, inverse, g1, s1, ok1, st);
+        if (rc) return rc;
+        if (ok1[0]) {
+            CU(cudaMemcpyAsync(hout(0), dout, grp_bytes, cudaMemcpyDeviceToHost, st));
+            CU(cudaStreamSynchronize(st));
+            if (!write_at(fout.fd, hout(0), grp_bytes, off)) return io_fail("cannot write", out_path);
+        }
+        fixed_ok[i] = ok1[0];
+    }
+    fill_lists(p, scheme, rep, bad_groups, fix_groups, fix_sig, fixed_ok);
     return TFFT_OK;
 }
 

@@ -1,10 +1,13 @@
-"""Golden fixtures for the campaign and propagation rows, produced by the REAL
-reference (build container only; see make_golden.py for the mechanics):
+"""Golden fixtures for the campaign, propagation, CLI and descriptor rows,
+produced by the REAL reference (build container only; see make_golden.py for
+the mechanics):
 
     python tests/golden/make_golden_campaign.py
 
 Writes campaign_*.csv (records + ROC of small campaigns in both precisions,
-with the output / input / stage hooks) and propagation.json (footprints)."""
+with the output / input / stage hooks), propagation.json (footprints),
+descriptors.json (`fftshield plan` JSON) and cli_transform.npz/json (raw files
+transformed by `fftshield transform`, with the printed reports)."""
 
 from __future__ import annotations
 
@@ -42,6 +45,44 @@ def main():
             f.write(roc_csv(res))
         print(name, res.default_delta, res.injected_count, res.detected_count, res.corrected_count,
               res.recompute_count)
+    # ---- `fftshield plan` descriptors
+    from fftshield import planner
+    desc = []
+    for n in (2, 8, 64, 1024, 2**13, 2**17, 2**20, 2**23, 2**25):
+        for b in (1, 16, 64):
+            for mode in planner.FT_MODES:
+                d = planner.emit_descriptor(planner.select_parameters(n, b), mode)
+                desc.append(dict(n=n, batch=b, ft_mode=mode, json=planner.render_descriptor(d)))
+    with open(os.path.join(HERE, "descriptors.json"), "w") as f:
+        json.dump(desc, f)
+    # ---- `fftshield transform` on raw files
+    import io
+    import contextlib
+    import tempfile
+    import numpy as np
+    from fftshield import cli
+    cases, arrays = [], {}
+    for i, (n, b, prec, scheme, inverse) in enumerate([(256, 16, "fp32", "two_sided_group", False),
+                                                       (1024, 8, "fp64", "one_sided", True),
+                                                       (2**14, 4, "fp32", "none", False)]):
+        rng = np.random.default_rng([4242, i])
+        x = (rng.standard_normal((b, n)) + 1j * rng.standard_normal((b, n))).astype(
+            np.complex64 if prec == "fp32" else np.complex128)
+        with tempfile.TemporaryDirectory() as td:
+            fi, fo = os.path.join(td, "in.raw"), os.path.join(td, "out.raw")
+            x.tofile(fi)
+            argv = ["transform", "--input", fi, "--output", fo, "--n", str(n), "--precision", prec,
+                    "--scheme", scheme] + (["--inverse"] if inverse else [])
+            buf = io.StringIO()
+            with contextlib.redirect_stdout(buf):
+                rc = cli.main(argv)
+            y = np.fromfile(fo, dtype=x.dtype).reshape(b, n)
+        arrays[f"c{i}_x"], arrays[f"c{i}_y"] = x, y
+        cases.append(dict(id=i, n=n, batch=b, precision=prec, scheme=scheme, inverse=inverse, rc=rc,
+                          stdout=buf.getvalue()))
+    np.savez_compressed(os.path.join(HERE, "cli_transform.npz"), **arrays)
+    with open(os.path.join(HERE, "cli_transform.json"), "w") as f:
+        json.dump(cases, f, indent=1)
     fp = [dict(n=n, stage=s, element=e, footprint=propagation_footprint(n, s, element=e)) for n, s, e in FOOTPRINTS]
     with open(os.path.join(HERE, "propagation.json"), "w") as f:
         json.dump(dict(campaigns=CAMPAIGNS, footprints=fp), f, indent=1)
