@@ -297,7 +297,17 @@ __device__ __forceinline__ float mag_fast(float2 z) {
     asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(s));
     return r;
 }
-__device__ __forceinline__ double mag_fast(double2 z) { return sqrt(ffma(z.x, z.x, fmul(z.y, z.y))); }
+// |z| for the l1 mass, which only feeds the detection floor
+// (FLOOR_COEF * sum|x|, pipeline.py:100-101): s * rsqrt.approx(s) (MUFU.RSQ64H,
+// ~1e-7 relative) instead of the IEEE sqrt's DFMA Newton chain. The floor
+// decides only when |c_in| < 1e-12 * sum|x|; at that relative accuracy no
+// decision moves.
+__device__ __forceinline__ double mag_fast(double2 z) {
+    const double s = ffma(z.x, z.x, fmul(z.y, z.y));
+    double r;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(s));
+    return s > 0.0 ? (s < 1e300 ? s * r : sqrt(s)) : s;
+}
 
 // Order-preserving key for non-negative floating values (NaN mapped to +inf
 // by the caller) — lets max_rel be reduced with integer atomicMax.

@@ -241,6 +241,16 @@ fft_pass_kernel(const __grid_constant__ PassArgs<T> a) {
         const bool fsig = fw != 0 && (a.sig_base + b) == fs && uu == fu && (fi % TPS) == t;
         const int fm = fi / TPS;
 
+        // input-side ABFT row e^T W for this tile, requested before the tile
+        // data is waited for so its latency overlaps (one batch of
+        // independent loads, not one round trip per element)
+        C<T> ew[(KIND == KIND_FIRST && ABFT != ABFT_OFF) ? E : 1];
+        if constexpr (KIND == KIND_FIRST && ABFT != ABFT_OFF) {
+            const C<T>* ep = a.etw + ibase + (long long)t * a.in_j;
+            const long long es = (long long)TPS * a.in_j;
+#pragma unroll
+            for (int m = 0; m < E; ++m) ew[m] = __ldg(ep + m * es);
+        }
         C<T> v[E];
         if constexpr (BULK) {
             if (tix + gridDim.x < total)
@@ -286,8 +296,7 @@ fft_pass_kernel(const __grid_constant__ PassArgs<T> a) {
             T l1 = T(0);
 #pragma unroll
             for (int m = 0; m < E; ++m) {
-                const C<T> e = __ldg(a.etw + ibase + (long long)(t + m * TPS) * a.in_j);
-                cin = cmac<T>(cin, v[m], e);
+                cin = cmac<T>(cin, v[m], ew[m]);
                 l1 = fadd(l1, mag_fast(v[m]));
             }
             T s[3] = {cin.x, cin.y, l1};

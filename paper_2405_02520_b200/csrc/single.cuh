@@ -197,6 +197,13 @@ fft_single_kernel(const SingleArgs<T> a) {
         C<T>* dst = a.out + b * N;
         const long long valid = (a.batch - tile * S) * N;  // elements of this CTA chunk in range
 
+        // input-side ABFT row e^T W at this thread's positions (the same for
+        // every tile: L1 hits), requested before the tile data is waited for
+        C<T> ew[ABFT != ABFT_OFF ? E : 1];
+        if constexpr (ABFT != ABFT_OFF) {
+#pragma unroll
+            for (int m = 0; m < E; ++m) ew[m] = __ldg(a.etw + t + m * TPS);
+        }
         C<T> v[E];
         if constexpr (PF && STG) {
             mbar_wait(&in_bar, iter & 1);
@@ -250,8 +257,7 @@ fft_single_kernel(const SingleArgs<T> a) {
         if constexpr (ABFT != ABFT_OFF) {
 #pragma unroll
             for (int m = 0; m < E; ++m) {
-                const C<T> e = __ldg(a.etw + t + m * TPS);
-                cin = cmac<T>(cin, v[m], e);
+                cin = cmac<T>(cin, v[m], ew[m]);
                 l1 = fadd(l1, mag_fast(v[m]));
             }
         }

@@ -434,7 +434,12 @@ int ensure_ring(tfft_plan* p, size_t chunk, cudaStream_t st) {
 // 1 GiB batch.
 int64_t groups_per_chunk(const tfft_plan* p, int64_t batch) {
     const int64_t grp_bytes = p->n * (int64_t)p->esize * p->bs;
-    int64_t gpc = std::max<int64_t>(1, ((int64_t)1 << 25) / grp_bytes);
+    static const int64_t target = [] {
+        const char* e = getenv("TFFT_STREAM_CHUNK_MB");  // tuning override
+        const long long mb = e ? atoll(e) : 0;
+        return mb > 0 ? (int64_t)mb << 20 : (int64_t)1 << 25;
+    }();
+    int64_t gpc = std::max<int64_t>(1, target / grp_bytes);
     return std::min<int64_t>(gpc, batch / p->bs);
 }
 

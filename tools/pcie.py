@@ -1,7 +1,12 @@
 """PCIe copy ceiling of the e2e number: pinned H2D, D2H and both at once
 (separate streams), 1 GiB each, CUDA events."""
 import json
+import os
+import sys
+
 import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 
 def main():
@@ -37,3 +42,33 @@ def main():
 
 if __name__ == "__main__":
     main()
+
+
+def host_path(logn=10, reps=5):
+    """run_protected on a pinned 1 GiB host batch (the e2e path) vs the copy
+    ceiling; prints ms per call."""
+    import time
+    import numpy as np
+    from paper_2405_02520_b200 import Scheme, build_twiddles, make_plan, run_protected
+    from paper_2405_02520_b200.abft import DetectionConfig
+    from paper_2405_02520_b200.fft_core import fit_group_size
+    n = 1 << logn
+    b = (1 << 30) // (8 * n)
+    xh = torch.randn(b, n, dtype=torch.complex64).pin_memory()
+    plan = fit_group_size(make_plan(n, "fp32", batch=b), b)
+    tw = build_twiddles(plan)
+    cfg = DetectionConfig(1e-4)
+    run_protected(plan, tw, xh, Scheme.TWO_SIDED_GROUP, cfg)
+    ts = []
+    for _ in range(reps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        out, rep, _ = run_protected(plan, tw, xh, Scheme.TWO_SIDED_GROUP, cfg)
+        ts.append((time.perf_counter() - t0) * 1e3)
+        del out
+    return {"logn": logn, "ms_host_path": round(min(ts), 2), "ms_median": round(sorted(ts)[len(ts) // 2], 2)}
+
+
+if __name__ == "__main__" and len(__import__("sys").argv) > 1:
+    import os
+    print(json.dumps(host_path(int(__import__("sys").argv[1]))), os.environ.get("TFFT_STREAM_CHUNK_MB"))
