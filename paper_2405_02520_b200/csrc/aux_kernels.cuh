@@ -47,6 +47,46 @@ dot_l1_kernel(const C<T>* __restrict__ x, long long n, const C<T>* __restrict__ 
     }
 }
 
+// Exact detection of signals the fused kernels could not decide from their
+// l1 upper bound (|c_in| below FLOOR_COEF * sum(|re|+|im|), so the floor may
+// matter): one CTA per listed signal recomputes c_in = x.etw, c_out = y.e and
+// sum|x| (IEEE hypot) and the reference's rel (pipeline.py:104-121).
+template <class T>
+__global__ void __launch_bounds__(AUX_THREADS)
+recheck_kernel(const C<T>* __restrict__ in, const C<T>* __restrict__ out, long long n,
+               const long long* __restrict__ sigs, const C<T>* __restrict__ etw,
+               const C<T>* __restrict__ values, T abs_floor, T floor_coef, double* __restrict__ rel) {
+    __shared__ T sh[AUX_THREADS / 32];
+    const long long sg = sigs[blockIdx.x];
+    const C<T>* x = in + sg * n;
+    const C<T>* y = out + sg * n;
+    C<T> cin = mk<T>(T(0), T(0)), cout = mk<T>(T(0), T(0));
+    T l1 = T(0);
+    const T hr = T(-0.5), hi = T(0.8660254037844386467637232);
+    for (long long k = threadIdx.x; k < n; k += blockDim.x) {
+        C<T> e;
+        if (values) e = values[k];
+        else {
+            const int cls = (int)(k % 3);
+            e = cls == 0 ? mk<T>(T(1), T(0)) : (cls == 1 ? mk<T>(hr, -hi) : mk<T>(hr, hi));
+        }
+        cout = cadd<T>(cout, cmul<T>(y[k], e));
+        cin = cadd<T>(cin, cmul<T>(x[k], etw[k]));
+        l1 = fadd(l1, cabs<T>(x[k]));
+    }
+    T a0 = block_sum(cin.x, sh), a1 = block_sum(cin.y, sh);
+    T a2 = block_sum(cout.x, sh), a3 = block_sum(cout.y, sh);
+    T a4 = block_sum(l1, sh);
+    if (threadIdx.x == 0) {
+        const C<T> raw = mk<T>(fsub(a0, a2), fsub(a1, a3));
+        const T fl = nanmax<T>(abs_floor, fmul(floor_coef, a4));
+        const T den = nanmax<T>(cabs<T>(mk<T>(a0, a1)), fl);
+        T r = cabs<T>(raw) / den;
+        if (!isfinite(r)) r = T(INFINITY);
+        rel[blockIdx.x] = (double)r;
+    }
+}
+
 // s0[k] = sum_b x_b[k] (sequential in b, like numpy's axis-0 sum),
 // s1[k] = sum_b (b+1) x_b[k] in complex128 (the reference promotes through
 // its float64 weights, pipeline.py:79-82).

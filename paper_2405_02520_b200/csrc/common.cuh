@@ -297,6 +297,9 @@ __device__ __forceinline__ float mag_fast(float2 z) {
     asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(s));
     return r;
 }
+// (|re|, |im|): per-element term of the l1 upper bound sum(|re| + |im|)
+template <class T> __device__ __forceinline__ C<T> cabs2(C<T> z) { return mk<T>(fabs(z.x), fabs(z.y)); }
+
 // |z| for the l1 mass, which only feeds the detection floor
 // (FLOOR_COEF * sum|x|, pipeline.py:100-101): s * rsqrt.approx(s) (MUFU.RSQ64H,
 // ~1e-7 relative) instead of the IEEE sqrt's DFMA Newton chain. The floor

@@ -293,13 +293,13 @@ fft_pass_kernel(const __grid_constant__ PassArgs<T> a) {
 
         if constexpr (KIND == KIND_FIRST && ABFT != ABFT_OFF) {
             C<T> cin = mk<T>(T(0), T(0));
-            T l1 = T(0);
+            C<T> l1p = mk<T>(T(0), T(0));  // l1 upper bound sum(|re| + |im|), see abft_decide
 #pragma unroll
             for (int m = 0; m < E; ++m) {
                 cin = cmac<T>(cin, v[m], ew[m]);
-                l1 = fadd(l1, mag_fast(v[m]));
+                l1p = cadd<T>(l1p, cabs2<T>(v[m]));
             }
-            T s[3] = {cin.x, cin.y, l1};
+            T s[3] = {cin.x, cin.y, fadd(l1p.x, l1p.y)};
             block_reduce<3>(s, red, THREADS / 32);
             if (threadIdx.x == 0) {
                 T* p = a.part + (b * a.tiles_per_sig + tsig) * 3;
@@ -356,18 +356,35 @@ fft_pass_kernel(const __grid_constant__ PassArgs<T> a) {
 
         if constexpr (KIND == KIND_LAST && ABFT != ABFT_OFF) {
             C<T> cout = mk<T>(T(0), T(0));
-            const T hr = T(-0.5), hq = T(0.8660254037844386467637232);
+            if constexpr (ABFT == ABFT_TABLE) {
 #pragma unroll
-            for (int m = 0; m < E; ++m) {
-                const long long f = obase + (long long)(t + m * TPS) * a.out_k;
-                C<T> e;
-                if constexpr (ABFT == ABFT_TABLE) {
-                    e = __ldg(a.values + f);
+                for (int m = 0; m < E; ++m)
+                    cout = cadd<T>(cout, cmul<T>(v[m], __ldg(a.values + obase + (long long)(t + m * TPS) * a.out_k)));
+            } else {
+                // Wang weights w3^(f mod 3) of output index f = obase + (t + m TPS) out_k:
+                // class(m) = (c0 + m*sc) mod 3 with one 64-bit residue per tile, so
+                // elements are summed per class (one packed add each) and weighted
+                // three times at the end
+                const int c0 = (int)((obase + (long long)t * a.out_k) % 3);
+                const int sc = (int)(((long long)TPS * a.out_k) % 3);
+                C<T> acc[3] = {mk<T>(T(0), T(0)), mk<T>(T(0), T(0)), mk<T>(T(0), T(0))};
+                if (sc == 1) {
+#pragma unroll
+                    for (int m = 0; m < E; ++m) acc[m % 3] = cadd<T>(acc[m % 3], v[m]);
+                } else if (sc == 2) {
+#pragma unroll
+                    for (int m = 0; m < E; ++m) acc[(2 * m) % 3] = cadd<T>(acc[(2 * m) % 3], v[m]);
                 } else {
-                    const int cls = (int)(f % 3);
-                    e = cls == 0 ? mk<T>(T(1), T(0)) : (cls == 1 ? mk<T>(hr, -hq) : mk<T>(hr, hq));
+#pragma unroll
+                    for (int m = 0; m < E; ++m) acc[0] = cadd<T>(acc[0], v[m]);
                 }
-                cout = cadd<T>(cout, cmul<T>(v[m], e));
+                const T hr = T(-0.5), hq = T(0.8660254037844386467637232);
+#pragma unroll
+                for (int r = 0; r < 3; ++r) {
+                    const int cls = (c0 + r) % 3;  // acc[r] holds class (c0 + r) mod 3
+                    const C<T> w = cls == 0 ? mk<T>(T(1), T(0)) : (cls == 1 ? mk<T>(hr, -hq) : mk<T>(hr, hq));
+                    cout = cadd<T>(cout, cmul<T>(acc[r], w));
+                }
             }
             T s[2] = {cout.x, cout.y};
             block_reduce<2>(s, red, THREADS / 32);
@@ -420,14 +437,14 @@ __global__ void __launch_bounds__(256) abft_finalize_kernel(const FinalArgs<T> a
             co_x = fadd(co_x, shfl_xor(co_x, off)); co_y = fadd(co_y, shfl_xor(co_y, off));
         }
         if (lane == 0) {
-            const C<T> raw = mk<T>(fsub(ci_x, co_x), fsub(ci_y, co_y));
-            const T fl = nanmax<T>(a.abs_floor, fmul(a.floor_coef, l1));
-            const T den = nanmax<T>(cabs<T>(mk<T>(ci_x, ci_y)), fl);
-            T rel = cabs<T>(raw) / den;
-            if (!isfinite(rel)) rel = T(INFINITY);
-            my_max = my_max > rel ? my_max : rel;
+            T rel, rel2;
+            bool flagged, recheck;
+            abft_decide<T>(ci_x, ci_y, co_x, co_y, l1, a.delta, a.abs_floor, a.floor_coef, true, rel, rel2,
+                           flagged, recheck);
+            if (recheck) rel = T(-1);  // sentinel: the host recomputes it exactly
+            else my_max = my_max > rel ? my_max : rel;
             if (a.rel_out) a.rel_out[b] = rel;
-            if (rel > a.delta) {
+            if (flagged || recheck) {
                 const int slot = atomicAdd(a.flag_count, 1);
                 if (slot < a.flag_cap) {
                     a.flag_sig[slot] = a.sig_base + b;

@@ -63,6 +63,53 @@ template <class T> __device__ __forceinline__ T nanmax(T a, T b) {
     return (a != a) ? a : ((b != b) ? b : (a > b ? a : b));
 }
 
+// Detection decision of one signal from its reduced checksums (reference
+// pipeline.py:104-121): rel = |c_in - c_out| / max(|c_in|, max(abs_floor,
+// FLOOR_COEF * sum|x|)), flag when rel > delta, non-finite -> inf.
+// The kernels carry l1b = sum(|re| + |im|), an upper bound of sum|x| within a
+// factor sqrt(2) that costs one packed add per element instead of a hypot.
+// Whenever the floor cannot matter (|c_in| >= FLOOR_COEF * l1b) or is exactly
+// abs_floor, the decision and rel are the reference's; otherwise (tiny
+// |c_in|, rare) the signal is sent back for an exact recheck (recheck_kernel).
+// A squared screen (no sqrt/div) clears the common case; anything near delta,
+// non-finite or out of range takes the exact arithmetic.
+template <class T>
+__device__ __forceinline__ void abft_decide(T r0, T r1, T r2, T r3, T l1b, T delta, T abs_floor, T coef,
+                                            bool want_rel, T& rel, T& rel2, bool& flagged, bool& recheck) {
+    flagged = false;
+    recheck = false;
+    rel = T(0);
+    rel2 = T(0);
+    const T dx = fsub(r0, r2), dy = fsub(r1, r3);
+    const T raw2 = ffma(dx, dx, fmul(dy, dy));
+    const T cin2 = ffma(r0, r0, fmul(r1, r1));
+    const T fb = fmul(coef, l1b);
+    const T flb = nanmax<T>(abs_floor, fb);
+    const bool floor_free = cin2 >= fmul(flb, flb);  // false for NaN
+    const bool abs_floor_exact = l1b == l1b && !(fb > abs_floor);
+    if (!floor_free && !abs_floor_exact) {
+        recheck = true;
+        return;
+    }
+    const T fl = floor_free ? T(0) : abs_floor;  // the exact floor term that can still matter
+    const T den2 = floor_free ? cin2 : nanmax<T>(cin2, fmul(fl, fl));
+    const T q = raw2 / den2;
+    const T d2 = fmul(delta, delta);
+    const bool in_range = den2 >= std::numeric_limits<T>::min() && den2 <= std::numeric_limits<T>::max() &&
+                          raw2 <= std::numeric_limits<T>::max();
+    if (in_range && q < T(0.81) * d2) {
+        rel2 = q;
+        if (want_rel) rel = sqrt(q);
+    } else {
+        const T cin = cabs<T>(mk<T>(r0, r1));
+        const T den = floor_free ? cin : nanmax<T>(cin, fl);
+        rel = cabs<T>(mk<T>(dx, dy)) / den;
+        if (!isfinite(rel)) rel = T(INFINITY);
+        flagged = rel > delta;
+        rel2 = rel * rel;
+    }
+}
+
 // Sum K values over the TPS consecutive threads of one signal (deterministic
 // tree). For TPS > 32 the per-warp partials go through `scratch` (K slots per
 // warp of the CTA) with a single barrier; only thread t == 0 of the signal
@@ -253,12 +300,12 @@ fft_single_kernel(const SingleArgs<T> a) {
 
         // ---- left-side input checksum on the pristine values
         C<T> cin = mk<T>(T(0), T(0));
-        T l1 = T(0);
+        C<T> l1p = mk<T>(T(0), T(0));  // (sum |re|, sum |im|): the l1 upper bound
         if constexpr (ABFT != ABFT_OFF) {
 #pragma unroll
             for (int m = 0; m < E; ++m) {
                 cin = cmac<T>(cin, v[m], ew[m]);
-                l1 = fadd(l1, mag_fast(v[m]));
+                l1p = cadd<T>(l1p, cabs2<T>(v[m]));
             }
         }
         int fw = a.f_where, fc = a.f_comp, fb = a.f_bit;
@@ -339,41 +386,20 @@ fft_single_kernel(const SingleArgs<T> a) {
                     cout = cadd<T>(cout, cmul<T>(v[m], e));
                 }
             }
-            T sums[5] = {cin.x, cin.y, cout.x, cout.y, l1};
+            T sums[5] = {cin.x, cin.y, cout.x, cout.y, fadd(l1p.x, l1p.y)};
             sig_sum<TPS>(sums, red, t);
-            const T r0 = sums[0], r1 = sums[1], r2 = sums[2], r3 = sums[3], r4 = sums[4];
-            bool flagged = false;
+            bool flagged = false, recheck = false;
             T rel = T(0);
             if (t == 0 && live) {
-                // squared screen: rel^2 = |raw|^2 / max(|c_in|, floor)^2 with no
-                // sqrt/hypot/div on the common path; anything near the
-                // threshold, non-finite or out of range takes the exact
-                // reference arithmetic (pipeline.py:116-121), so decisions match.
-                const T dx = fsub(r0, r2), dy = fsub(r1, r3);
-                const T raw2 = ffma(dx, dx, fmul(dy, dy));
-                const T cin2 = ffma(r0, r0, fmul(r1, r1));
-                const T fl = nanmax<T>(a.abs_floor, fmul(a.floor_coef, r4));
-                const T den2 = nanmax<T>(cin2, fmul(fl, fl));
-                const T q = raw2 / den2;
-                const T d2 = fmul(a.delta, a.delta);
-                const bool in_range = den2 >= std::numeric_limits<T>::min() &&
-                                      den2 <= std::numeric_limits<T>::max() &&
-                                      raw2 <= std::numeric_limits<T>::max();
                 T rel2;
-                if (in_range && q < T(0.81) * d2) {
-                    rel2 = q;
-                    if (a.rel_out) rel = sqrt(q);
-                } else {
-                    const T den = nanmax<T>(cabs<T>(mk<T>(r0, r1)), fl);
-                    rel = cabs<T>(mk<T>(dx, dy)) / den;
-                    if (!isfinite(rel)) rel = T(INFINITY);
-                    flagged = rel > a.delta;
-                    rel2 = rel * rel;
-                }
-                my_max = my_max > rel2 ? my_max : rel2;  // squared; sqrt once per CTA
+                abft_decide<T>(sums[0], sums[1], sums[2], sums[3], sums[4], a.delta, a.abs_floor, a.floor_coef,
+                               a.rel_out != nullptr, rel, rel2, flagged, recheck);
+                if (recheck) rel = T(-1);  // sentinel: the host recomputes it exactly
+                else my_max = my_max > rel2 ? my_max : rel2;  // squared; sqrt once per CTA
                 if (a.rel_out) a.rel_out[b] = rel;
+                flagged = flagged || recheck;
             }
-            // warp-aggregated append of flagged signals (rare)
+            // warp-aggregated append of flagged / recheck signals (rare)
             const unsigned ball = __ballot_sync(0xffffffffu, flagged);
             if (ball) {
                 const int lane = threadIdx.x & 31;

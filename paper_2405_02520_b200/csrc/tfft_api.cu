@@ -13,6 +13,7 @@
 #include <condition_variable>
 #include <cstdio>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <mutex>
 #include <string>
@@ -757,24 +758,56 @@ int tfft_protect_launch(tfft_plan* p, const void* in, void* out, int64_t batch, 
 
 namespace {
 
+// Exact rel of `sigs` (indices into the device buffers in/out) for the
+// signals the kernels sent back (recheck_kernel).
+int recheck_device(tfft_plan* p, const void* in, const void* out, const std::vector<long long>& sigs,
+                   const void* etw, const void* values, double abs_floor, std::vector<double>& rel,
+                   cudaStream_t st) {
+    rel.assign(sigs.size(), 0.0);
+    if (sigs.empty()) return TFFT_OK;
+    const size_t k = sigs.size();
+    int rc = ensure_scratch(p, k * (sizeof(long long) + sizeof(double)));
+    if (rc) return rc;
+    long long* d_sig = (long long*)p->d_scratch;
+    double* d_rel = (double*)(d_sig + k);
+    CU(cudaMemcpyAsync(d_sig, sigs.data(), k * sizeof(long long), cudaMemcpyHostToDevice, st));
+    if (p->prec == TFFT_FP32)
+        recheck_kernel<float><<<(unsigned)k, AUX_THREADS, 0, st>>>(
+            (const float2*)in, (const float2*)out, p->n, d_sig, (const float2*)etw, (const float2*)values,
+            (float)abs_floor, 1e-6f, d_rel);
+    else
+        recheck_kernel<double><<<(unsigned)k, AUX_THREADS, 0, st>>>(
+            (const double2*)in, (const double2*)out, p->n, d_sig, (const double2*)etw, (const double2*)values,
+            abs_floor, 1e-12, d_rel);
+    CU(cudaGetLastError());
+    CU(cudaMemcpyAsync(rel.data(), d_rel, k * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    return TFFT_OK;
+}
+
+// Resolves the exact rel of recheck signals (global indices) -> rel.
+using RecheckFn = std::function<int(const std::vector<long long>&, std::vector<double>&)>;
+
 // Detection summary of the launches since the last counter reset: max rel
 // discrepancy and the flagged (global signal, rel) list, sorted like the
-// reference's group loop.
+// reference's group loop. Entries with the recheck sentinel (rel < 0) are
+// resolved exactly through `resolve` and merged.
 int read_summary(tfft_plan* p, int64_t batch, cudaStream_t st, tfft_report* rep,
-                 std::vector<std::pair<long long, double>>& flags) {
+                 std::vector<std::pair<long long, double>>& flags, double delta, const RecheckFn& resolve,
+                 std::vector<std::pair<long long, double>>* rechecked = nullptr) {
     CU(cudaEventSynchronize(p->ev_done));
     const int64_t nflag = std::min<int64_t>(p->h_cnt->flag_count, batch);
+    double max_rel;
     if (p->prec == TFFT_FP32) {
         unsigned int k = (unsigned int)(p->h_cnt->max_key & 0xffffffffull);
         float f;
         memcpy(&f, &k, 4);
-        rep->max_rel_discrepancy = f;
+        max_rel = f;
     } else {
-        double d;
-        memcpy(&d, &p->h_cnt->max_key, 8);
-        rep->max_rel_discrepancy = d;
+        memcpy(&max_rel, &p->h_cnt->max_key, 8);
     }
     flags.clear();
+    std::vector<long long> rsig;
     if (nflag > 0) {
         std::vector<long long> sig(nflag);
         CU(cudaMemcpyAsync(sig.data(), p->d_flag_sig, nflag * sizeof(long long), cudaMemcpyDeviceToHost, st));
@@ -788,9 +821,26 @@ int read_summary(tfft_plan* p, int64_t batch, cudaStream_t st, tfft_report* rep,
             CU(cudaMemcpyAsync(rel.data(), p->d_flag_rel, nflag * sizeof(double), cudaMemcpyDeviceToHost, st));
             CU(cudaStreamSynchronize(st));
         }
-        for (int64_t i = 0; i < nflag; ++i) flags.emplace_back(sig[i], rel[i]);
-        std::sort(flags.begin(), flags.end());
+        for (int64_t i = 0; i < nflag; ++i) {
+            if (rel[i] < 0) rsig.push_back(sig[i]);
+            else flags.emplace_back(sig[i], rel[i]);
+        }
     }
+    if (!rsig.empty()) {
+        std::sort(rsig.begin(), rsig.end());
+        std::vector<double> rr;
+        int rc = resolve(rsig, rr);
+        if (rc) return rc;
+        for (size_t i = 0; i < rsig.size(); ++i) {
+            const double r = rr[i];
+            if (r > max_rel || r != r) max_rel = r != r ? INFINITY : r;
+            const bool hit = p->prec == TFFT_FP32 ? (float)r > (float)delta : r > delta;
+            if (hit) flags.emplace_back(rsig[i], r);
+            if (rechecked) rechecked->emplace_back(rsig[i], r);
+        }
+    }
+    std::sort(flags.begin(), flags.end());
+    rep->max_rel_discrepancy = max_rel;
     // flagged list, in (group, signal) order like the reference's loop
     rep->n_flagged = (int64_t)flags.size();
     for (size_t i = 0; i < flags.size() && (int64_t)i < rep->flagged_cap; ++i) {
@@ -928,7 +978,10 @@ int tfft_protect_finish(tfft_plan* p, const void* in, void* out, int64_t batch, 
     if (scheme == TFFT_SCHEME_NONE) return TFFT_OK;
     if (!p->ev_done) return fail(TFFT_EINVAL, "tfft_protect_finish without tfft_protect_launch");
     std::vector<std::pair<long long, double>> flags;
-    rc = read_summary(p, batch, st, rep, flags);
+    RecheckFn resolve = [&](const std::vector<long long>& sg, std::vector<double>& rr) {
+        return recheck_device(p, in, out, sg, etw, values, abs_floor, rr, st);
+    };
+    rc = read_summary(p, batch, st, rep, flags, delta, resolve);
     if (rc) return rc;
     std::vector<int64_t> bad_groups, fix_groups, fix_sig;
     decide(p, flags, bad_groups, fix_groups, fix_sig);
@@ -1074,7 +1127,21 @@ int tfft_run_protected_host(tfft_plan* p, const void* in, void* out, int64_t bat
     CU(cudaEventRecord(p->ev_done, st));
     CU(cudaStreamSynchronize(st));
     std::vector<std::pair<long long, double>> flags;
-    rc = read_summary(p, batch, st, rep, flags);
+    RecheckFn resolve = [&](const std::vector<long long>& sg, std::vector<double>& rr) {
+        rr.assign(sg.size(), 0.0);
+        char* din = (char*)p->ring;
+        char* dout = din + p->ring_chunk;
+        for (size_t i = 0; i < sg.size(); ++i) {  // rare: stage the signal's input and output rows
+            CU(cudaMemcpyAsync(din, (const char*)in + sg[i] * sig_bytes, sig_bytes, cudaMemcpyHostToDevice, st));
+            CU(cudaMemcpyAsync(dout, (const char*)out + sg[i] * sig_bytes, sig_bytes, cudaMemcpyHostToDevice, st));
+            std::vector<double> r1;
+            int rc2 = recheck_device(p, din, dout, {0}, etw, values, abs_floor, r1, st);
+            if (rc2) return rc2;
+            rr[i] = r1[0];
+        }
+        return (int)TFFT_OK;
+    };
+    rc = read_summary(p, batch, st, rep, flags, delta, resolve);
     if (rc) return rc;
     std::vector<int64_t> bad_groups, fix_groups, fix_sig;
     decide(p, flags, bad_groups, fix_groups, fix_sig);
@@ -1185,10 +1252,21 @@ int tfft_run_campaign(tfft_plan* p, const void* in, void* out, int64_t runs, int
     CU(cudaMemcpyAsync(p->h_cnt, p->d_cnt, sizeof(Counters), cudaMemcpyDeviceToHost, st));
     if (!p->ev_done) CU(cudaEventCreateWithFlags(&p->ev_done, cudaEventDisableTiming));
     CU(cudaEventRecord(p->ev_done, st));
+    std::vector<std::pair<long long, double>> flags;
+    std::vector<std::pair<long long, double>> rechecked;
+    RecheckFn resolve = [&](const std::vector<long long>& sg, std::vector<double>& rr) {
+        return recheck_device(p, in, out, sg, etw, values, abs_floor, rr, st);
+    };
+    rc = read_summary(p, batch, st, rep, flags, delta, resolve, &rechecked);
+    if (rc) return rc;
     // per-run max discrepancy (protected.py:124-126 max over the run's groups)
     std::vector<char> rel((size_t)batch * tb);
     CU(cudaMemcpyAsync(rel.data(), p->d_rel, batch * tb, cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));
+    for (const auto& rc_ : rechecked) {  // exact values of the recheck sentinels
+        if (tb == 4) ((float*)rel.data())[rc_.first] = (float)rc_.second;
+        else ((double*)rel.data())[rc_.first] = rc_.second;
+    }
     for (int64_t r = 0; r < runs; ++r) {
         double mx = 0.0;
         for (int64_t i = r * run_batch; i < (r + 1) * run_batch; ++i) {
@@ -1197,9 +1275,6 @@ int tfft_run_campaign(tfft_plan* p, const void* in, void* out, int64_t runs, int
         }
         run_max_rel[r] = mx;
     }
-    std::vector<std::pair<long long, double>> flags;
-    rc = read_summary(p, batch, st, rep, flags);
-    if (rc) return rc;
     std::vector<int64_t> bad_groups, fix_groups, fix_sig;
     decide(p, flags, bad_groups, fix_groups, fix_sig);
     std::vector<char> fixed_ok;
@@ -1408,7 +1483,27 @@ int tfft_run_protected_file(tfft_plan* p, const char* in_path, const char* out_p
     CU(cudaMemcpyAsync(p->h_cnt, p->d_cnt, sizeof(Counters), cudaMemcpyDeviceToHost, st));
     CU(cudaEventRecord(p->ev_done, st));
     std::vector<std::pair<long long, double>> flags;
-    rc = read_summary(p, batch, st, rep, flags);
+    RecheckFn resolve = [&](const std::vector<long long>& sg, std::vector<double>& rr) {
+        rr.assign(sg.size(), 0.0);
+        char* din = (char*)p->ring;
+        char* dout = din + p->ring_chunk;
+        Fd fo;
+        fo.fd = open(out_path, O_RDONLY);
+        if (fo.fd < 0) return io_fail("cannot reopen", out_path);
+        for (size_t i = 0; i < sg.size(); ++i) {  // rare: re-stage the signal's rows from the files
+            const off_t off = (off_t)(sg[i] * sig_bytes);
+            if (!read_at(fin.fd, hin(0), sig_bytes, off)) return io_fail("cannot read", in_path);
+            if (!read_at(fo.fd, hout(0), sig_bytes, off)) return io_fail("cannot read", out_path);
+            CU(cudaMemcpyAsync(din, hin(0), sig_bytes, cudaMemcpyHostToDevice, st));
+            CU(cudaMemcpyAsync(dout, hout(0), sig_bytes, cudaMemcpyHostToDevice, st));
+            std::vector<double> r1;
+            int rc2 = recheck_device(p, din, dout, {0}, etw, values, abs_floor, r1, st);
+            if (rc2) return rc2;
+            rr[i] = r1[0];
+        }
+        return (int)TFFT_OK;
+    };
+    rc = read_summary(p, batch, st, rep, flags, delta, resolve);
     if (rc) return rc;
     std::vector<int64_t> bad_groups, fix_groups, fix_sig;
     decide(p, flags, bad_groups, fix_groups, fix_sig);

@@ -262,3 +262,35 @@ def test_host_streaming_matches_device_path(n, prec, batch, scheme):
     assert inj.fired
     if scheme != "none":
         assert [c["signal"] for c in rh.corrected] == [batch - 3]
+
+
+@pytest.mark.parametrize("n,prec,device_input", [(1024, "fp32", True), (1 << 15, "fp64", True),
+                                                 (256, "fp32", False)])
+def test_floor_recheck_path_matches_oracle(n, prec, device_input):
+    """Signals with c_in ~ 0 (orthogonal to e^T W) make the detection floor
+    FLOOR_COEF * sum|x| decide; the kernels cannot settle that from their l1
+    upper bound and send them to the exact recheck. Their flags and rel must
+    be the reference's (oracle port), mixed with ordinary signals."""
+    from oracle import port as P
+    dt = np.complex64 if prec == "fp32" else np.complex128
+    rng = np.random.default_rng(21)
+    b = 8
+    x = (rng.standard_normal((b, n)) + 1j * rng.standard_normal((b, n)))
+    etw = P.encoding_for("wang", n).etw
+    for s in (1, 2, 5):  # project out the checksum direction
+        x[s] -= (x[s] @ etw) * np.conj(etw) / np.vdot(etw, etw).real
+    x = x.astype(dt)
+    plan = fit_group_size(make_plan(n, prec, batch=b), 1)
+    delta = 1e-4 if prec == "fp32" else 1e-9
+    xin = torch.from_numpy(x).cuda() if device_input else x
+    _, rep, _ = run_protected(plan, build_twiddles(plan), xin, Scheme.TWO_SIDED_GROUP, DetectionConfig(delta))
+    op = P.shrink_bs(P.plan_for(n, prec, batch=b), 1)
+    _, orep, _ = P.protected(op, P.twiddles_for(op), x, "two_sided_group", delta=delta)
+    assert [f["signal"] for f in rep.flagged] == [f["signal"] for f in orep["flagged"]]
+    assert {1, 2, 5} <= {f["signal"] for f in rep.flagged}
+    # c_in and c_out of these signals are rounding noise of two different FFT
+    # implementations: the values agree in magnitude, far above delta
+    for mine, theirs in zip(rep.flagged, orep["flagged"]):
+        assert mine["discrepancy"] > 10 * delta and theirs["discrepancy"] > 10 * delta
+        assert 0.2 < mine["discrepancy"] / theirs["discrepancy"] < 5
+    assert rep.max_rel_discrepancy > 0 and math.isfinite(rep.max_rel_discrepancy)
