@@ -91,8 +91,8 @@ SINGLE_CANDIDATES = {
 # tuned winners (index into SINGLE_CANDIDATES[prec][logn]); missing -> 0.
 # Source: tools/tune.py on a B200, ABFT on, 1 GiB batches (profiles/tune_r01.json).
 SINGLE_CHOICE = {
-    "fp32": {1: 1, 2: 1, 3: 4, 4: 5, 5: 1, 6: 1, 7: 0, 8: 4, 9: 0, 10: 1, 11: 5, 12: 5, 13: 5},
-    "fp64": {1: 1, 2: 1, 3: 3, 4: 3, 5: 1, 6: 1, 7: 3, 8: 2, 9: 3, 10: 2, 11: 1, 12: 1, 13: 0},
+    "fp32": {1: 1, 2: 1, 3: 4, 4: 5, 5: 5, 6: 1, 7: 0, 8: 4, 9: 0, 10: 1, 11: 5, 12: 5, 13: 0},
+    "fp64": {1: 1, 2: 2, 3: 3, 4: 4, 5: 4, 6: 4, 7: 0, 8: 2, 9: 1, 10: 2, 11: 1, 12: 3, 13: 0},
 }
 ELEM_BYTES = {"fp32": 8, "fp64": 16}
 CTYPE = {"fp32": "float", "fp64": "double"}
