@@ -196,6 +196,19 @@ int tfft_detect(tfft_plan *plan, const void *yg, int64_t bs, const void *values,
 int tfft_correct_signal(tfft_plan *plan, const void *s0, const void *yg, int64_t bs,
                         int64_t f, void *fixed, int inverse, void *stream);
 
+/* abft/element.py:33-92 two_sided_element on one r x B tile (1 <= r <= 32),
+ * complex128 device arrays, row-major (r, B). _encode: y[:, j] = DFT_r of
+ * column j, row_in[j] = etw_row . x[:, j] (row side), xe = x @ vals_col
+ * (column side). _verify (after any injection into y): rel[j] per column,
+ * result (host int[3]) = {0 clean | 1 corrected | 2 several columns flagged |
+ * 3 row/column disagreements inconsistent, row, col}; a corrected y is
+ * fixed in place. Blocks until result is filled. */
+int tfft_element_encode(int r, int64_t B, const void *x, void *y, const void *etw_row,
+                        const void *vals_col, void *row_in, void *xe, void *stream);
+int tfft_element_verify(int r, int64_t B, void *y, const void *row_in, const void *xe,
+                        const void *vals_row, const void *vals_col, double delta, double abs_floor,
+                        void *rel, int32_t *result, void *stream);
+
 /* fault_lab/bits.py:11-27,48-53 flip_bit/apply_fault on device memory:
  * XOR bit `bit` of real word `word` (2*element + component) of buf. */
 int tfft_flip_bit(void *buf, int64_t word, int bit, int dtype_bytes, void *stream);

@@ -69,6 +69,9 @@ SIGNATURES = {
     "tfft_encode_group": (_INT, [_VP, _VP, _I64, _VP, _VP, _VP, _VP, _VP, _VP]),
     "tfft_detect": (_INT, [_VP, _VP, _I64, _VP, _VP, _VP, _DBL, _VP, _VP, _VP]),
     "tfft_correct_signal": (_INT, [_VP, _VP, _VP, _I64, _I64, _VP, _INT, _VP]),
+    "tfft_element_encode": (_INT, [_INT, _I64, _VP, _VP, _VP, _VP, _VP, _VP, _VP]),
+    "tfft_element_verify": (_INT, [_INT, _I64, _VP, _VP, _VP, _VP, _VP, _DBL, _DBL, _VP,
+                                   ctypes.POINTER(ctypes.c_int32), _VP]),
     "tfft_flip_bit": (_INT, [_VP, _I64, _INT, _INT, _VP]),
     "tfft_execute_stage": (_INT, [_VP, _INT, _VP, _VP, _I64, _INT, _VP]),
     "tfft_scale": (_INT, [_VP, _I64, _INT, _DBL, _VP]),

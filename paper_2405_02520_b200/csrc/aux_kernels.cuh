@@ -246,4 +246,130 @@ __global__ void flip_word_kernel(void* buf, long long word, int bit, int bytes) 
     }
 }
 
+
+// ---------------------------------------------------------------- element level
+// Element-level two-sided check of one r x B tile (reference abft/element.py:
+// 33-92), complex128 like the reference. Tile layout: row-major (r, B), column
+// j is one signal's r-point slice.
+
+// y[:, j] = DFT_r(x[:, j]); row_in[j] = etw_row . x[:, j]; xe[i] = x[i, :] . vals_col
+__global__ void element_encode_kernel(int r, long long B, const double2* __restrict__ x,
+                                      const double2* __restrict__ etw_row, const double2* __restrict__ vals_col,
+                                      double2* __restrict__ y, double2* __restrict__ row_in,
+                                      double2* __restrict__ xe) {
+    __shared__ double2 root[32];
+    if (threadIdx.x < r) {
+        double s, c;
+        sincospi(-2.0 * threadIdx.x / r, &s, &c);  // w_r^m, exactly rounded
+        root[threadIdx.x] = make_double2(c, s);
+    }
+    __syncthreads();
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < B; j += stride) {
+        double2 ri = make_double2(0.0, 0.0);
+        for (int i = 0; i < r; ++i) ri = cadd<double>(ri, cmul<double>(etw_row[i], x[i * B + j]));
+        row_in[j] = ri;
+        for (int k = 0; k < r; ++k) {
+            double2 acc = make_double2(0.0, 0.0);
+            for (int i = 0; i < r; ++i) acc = cadd<double>(acc, cmul<double>(x[i * B + j], root[(i * k) % r]));
+            y[k * B + j] = acc;
+        }
+    }
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < r; i += stride) {
+        double2 acc = make_double2(0.0, 0.0);
+        for (long long j = 0; j < B; ++j) acc = cadd<double>(acc, cmul<double>(x[i * B + j], vals_col[j]));
+        xe[i] = acc;
+    }
+}
+
+__device__ __forceinline__ double2 cdiv_d(double2 a, double2 b) {
+    const double d = b.x * b.x + b.y * b.y;
+    return make_double2((a.x * b.x + a.y * b.y) / d, (a.y * b.x - a.x * b.y) / d);
+}
+__device__ __forceinline__ bool cfinite(double2 z) { return isfinite(z.x) && isfinite(z.y); }
+
+// Row side locates the column (signal), column side the row; one CTA.
+// result[0]: 0 clean, 1 corrected, 2 several columns flagged, 3 row/column
+// disagreements inconsistent; result[1..2] = (row, col) when corrected.
+__global__ void __launch_bounds__(AUX_THREADS)
+element_verify_kernel(int r, long long B, double2* __restrict__ y, const double2* __restrict__ row_in,
+                      const double2* __restrict__ xe, const double2* __restrict__ vals_row,
+                      const double2* __restrict__ vals_col, double delta, double abs_floor,
+                      double* __restrict__ rel, int* __restrict__ result) {
+    __shared__ int nflag, col;
+    __shared__ double2 d_row_j, dcol[32], wxe[32];
+    if (threadIdx.x == 0) { nflag = 0; col = -1; }
+    __syncthreads();
+    for (long long j = threadIdx.x; j < B; j += blockDim.x) {
+        double2 c = make_double2(0.0, 0.0);
+        bool fin = true;
+        for (int i = 0; i < r; ++i) {
+            const double2 v = y[i * B + j];
+            fin = fin && cfinite(v);
+            c = cadd<double>(c, cmul<double>(vals_row[i], v));
+        }
+        const double2 d = make_double2(row_in[j].x - c.x, row_in[j].y - c.y);
+        const double den = fmax(hypot(row_in[j].x, row_in[j].y), abs_floor);
+        double q = hypot(d.x, d.y) / (den > 0 ? den : 1.0);
+        if (!fin || !isfinite(q)) q = INFINITY;
+        rel[j] = q;
+        if (q > delta) {
+            atomicAdd(&nflag, 1);
+            atomicMax(&col, (int)j);
+            d_row_j = d;  // meaningful when exactly one column is flagged
+        }
+    }
+    __syncthreads();
+    if (nflag == 0 || nflag > 1) {
+        if (threadIdx.x == 0) result[0] = nflag == 0 ? 0 : 2;
+        return;
+    }
+    const int j = col;
+    // column side: d_col = DFT_r(xe) - y @ vals_col
+    if (threadIdx.x < r) {
+        const int i = threadIdx.x;
+        double2 w = make_double2(0.0, 0.0);
+        for (int m = 0; m < r; ++m) {
+            double s, c;
+            sincospi(-2.0 * ((m * i) % r) / r, &s, &c);
+            w = cadd<double>(w, cmul<double>(xe[m], make_double2(c, s)));
+        }
+        wxe[i] = w;
+        double2 acc = make_double2(0.0, 0.0);
+        for (long long b = 0; b < B; ++b) acc = cadd<double>(acc, cmul<double>(y[i * B + b], vals_col[b]));
+        dcol[i] = make_double2(w.x - acc.x, w.y - acc.y);
+    }
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    int bi = 0;
+    double best = -1.0;
+    for (int i = 0; i < r; ++i) {  // first maximal |d_col|, non-finite counts as inf
+        const double a = cfinite(dcol[i]) ? hypot(dcol[i].x, dcol[i].y) : INFINITY;
+        if (a > best) { best = a; bi = i; }
+    }
+    const double2 fix = cdiv_d(dcol[bi], vals_col[j]);
+    const double2 eps_col = make_double2(-fix.x, -fix.y);
+    const double2 er = cdiv_d(d_row_j, vals_row[bi]);
+    const double2 eps_row = make_double2(-er.x, -er.y);
+    if (cfinite(eps_col) && cfinite(eps_row)) {
+        const double gap = hypot(eps_row.x - eps_col.x, eps_row.y - eps_col.y);
+        if (gap > delta * fmax(hypot(eps_col.x, eps_col.y), abs_floor)) {
+            result[0] = 3;
+            return;
+        }
+    }
+    double2& t = y[bi * B + j];
+    if (cfinite(t)) {
+        t = make_double2(t.x + fix.x, t.y + fix.y);
+    } else {
+        double2 others = make_double2(0.0, 0.0);
+        for (long long b = 0; b < B; ++b)
+            if (b != j) others = cadd<double>(others, cmul<double>(y[bi * B + b], vals_col[b]));
+        t = cdiv_d(make_double2(wxe[bi].x - others.x, wxe[bi].y - others.y), vals_col[j]);
+    }
+    result[0] = 1;
+    result[1] = bi;
+    result[2] = j;
+}
+
 }  // namespace tfft

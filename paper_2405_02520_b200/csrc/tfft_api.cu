@@ -1539,3 +1539,39 @@ int tfft_run_protected_file(tfft_plan* p, const char* in_path, const char* out_p
 }
 
 }  // extern "C"
+
+extern "C" {
+
+int tfft_element_encode(int r, int64_t B, const void* x, void* y, const void* etw_row, const void* vals_col,
+                        void* row_in, void* xe, void* stream) {
+    if (r < 1 || r > 32 || B < 1) return fail(TFFT_EINVAL, "tile must be r x B with 1 <= r <= 32");
+    if (!x || !y || !etw_row || !vals_col || !row_in || !xe) return fail(TFFT_EINVAL, "null buffer");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int grid = (int)std::min<long long>((B + 127) / 128, 1024);
+    element_encode_kernel<<<std::max(grid, 1), 128, 0, st>>>(r, B, (const double2*)x, (const double2*)etw_row,
+                                                               (const double2*)vals_col, (double2*)y,
+                                                               (double2*)row_in, (double2*)xe);
+    CU(cudaGetLastError());
+    return TFFT_OK;
+}
+
+int tfft_element_verify(int r, int64_t B, void* y, const void* row_in, const void* xe, const void* vals_row,
+                        const void* vals_col, double delta, double abs_floor, void* rel, int32_t* result,
+                        void* stream) {
+    if (r < 1 || r > 32 || B < 1) return fail(TFFT_EINVAL, "tile must be r x B with 1 <= r <= 32");
+    if (!y || !row_in || !xe || !vals_row || !vals_col || !rel || !result) return fail(TFFT_EINVAL, "null buffer");
+    cudaStream_t st = (cudaStream_t)stream;
+    int* d_res = nullptr;
+    CU(cudaMallocAsync((void**)&d_res, 3 * sizeof(int), st));
+    CU(cudaMemsetAsync(d_res, 0, 3 * sizeof(int), st));
+    element_verify_kernel<<<1, AUX_THREADS, 0, st>>>(r, B, (double2*)y, (const double2*)row_in, (const double2*)xe,
+                                                     (const double2*)vals_row, (const double2*)vals_col, delta,
+                                                     abs_floor, (double*)rel, d_res);
+    CU(cudaGetLastError());
+    CU(cudaMemcpyAsync(result, d_res, 3 * sizeof(int), cudaMemcpyDeviceToHost, st));
+    CU(cudaFreeAsync(d_res, st));
+    CU(cudaStreamSynchronize(st));
+    return TFFT_OK;
+}
+
+}  // extern "C"

@@ -83,6 +83,47 @@ def main():
     np.savez_compressed(os.path.join(HERE, "cli_transform.npz"), **arrays)
     with open(os.path.join(HERE, "cli_transform.json"), "w") as f:
         json.dump(cases, f, indent=1)
+    # ---- element-level two-sided tiles (abft/element.py)
+    from fftshield.abft import DetectionConfig, UnrecoverableError, make_encoding, two_sided_element
+    el_cases, el_arrays = [], {}
+    specs = [  # (r, B, row enc, col enc, delta, abs_floor, edits [(i, j, kind, value)])
+        (8, 8, "ones", "linear", 1e-6, 1e-12, []),
+        (4, 4, "ones", "linear", 1e-6, 1e-12, [(3, 2, "add", 7.0)]),
+        (16, 5, "wang", "linear", 1e-9, 1e-12, [(5, 1, "add", 3.0 - 2.0j)]),
+        (8, 6, "wang", "ones", 1e-9, 1e-12, [(2, 3, "set", complex(np.inf, 0.0))]),
+        (8, 8, "ones", "linear", 1e-6, 1e-12, [(1, 1, "add", 5.0), (2, 6, "add", 4.0)]),
+        (8, 8, "ones", "linear", 1e-6, 1e-12, [(1, 3, "add", 5.0), (6, 3, "add", -2.0j)]),
+        (32, 32, "wang", "wang", 1e-9, 1e-12, [(31, 0, "add", 1e-3)]),
+        (2, 3, "linear", "linear", 1e-6, 0.0, [(0, 2, "add", 1.0)]),
+    ]
+    for cid, (r, b, er, ec, delta, floor, edits) in enumerate(specs):
+        rng = np.random.default_rng([99, cid])
+        x = rng.standard_normal((r, b)) + 1j * rng.standard_normal((r, b))
+
+        def inject(y, _e=edits):
+            for i, j, kind, val in _e:
+                if kind == "add":
+                    y[i, j] += val
+                else:
+                    y[i, j] = val
+
+        try:
+            y, rep = two_sided_element(r, x, make_encoding(er, r), make_encoding(ec, b),
+                                       DetectionConfig(delta=delta, abs_floor=floor),
+                                       inject=inject if edits else None)
+            outcome = dict(error=None, located=list(rep.located) if rep.located else None,
+                           corrected=rep.corrected)
+            el_arrays[f"e{cid}_y"] = y
+            el_arrays[f"e{cid}_rel"] = rep.col_discrepancies
+        except UnrecoverableError as exc:
+            outcome = dict(error=str(exc), located=None, corrected=False)
+        el_arrays[f"e{cid}_x"] = x
+        el_cases.append(dict(id=cid, r=r, b=b, enc_row=er, enc_col=ec, delta=delta, abs_floor=floor,
+                             edits=[[i, j, k, [complex(v).real, complex(v).imag]] for i, j, k, v in edits],
+                             **outcome))
+    np.savez_compressed(os.path.join(HERE, "element.npz"), **el_arrays)
+    with open(os.path.join(HERE, "element.json"), "w") as f:
+        json.dump(el_cases, f, indent=1)
     fp = [dict(n=n, stage=s, element=e, footprint=propagation_footprint(n, s, element=e)) for n, s, e in FOOTPRINTS]
     with open(os.path.join(HERE, "propagation.json"), "w") as f:
         json.dump(dict(campaigns=CAMPAIGNS, footprints=fp), f, indent=1)
