@@ -51,8 +51,14 @@ def peaks():
 
 # ------------------------------------------------------------------ clocks
 class ClockSampler:
-    """Samples SM clocks and throttle reasons through NVML every 50 ms while
-    the timed region runs (the recipe's nvidia-smi clocks line, in-process)."""
+    """Samples SM clocks and throttle reasons through NVML every 5 ms while
+    the timed region runs (the recipe's nvidia-smi clocks line, in-process).
+    NVML is initialised before the timed region and one sample is taken at
+    start and at stop, so even a short region has samples."""
+
+    NAMES = {"HwSlowdown": "hw_slowdown", "HwThermalSlowdown": "hw_thermal_slowdown",
+             "SwThermalSlowdown": "sw_thermal_slowdown", "SwPowerCap": "sw_power_cap",
+             "HwPowerBrakeSlowdown": "hw_power_brake"}
 
     def __init__(self, index, period=0.005):
         self.index = index
@@ -63,30 +69,36 @@ class ClockSampler:
         self._stop = threading.Event()
         self._thr = None
         self.err = None
-
-    def _run(self):
+        self._nv = self._h = None
         try:
             import pynvml as nv
             nv.nvmlInit()
-            h = nv.nvmlDeviceGetHandleByIndex(self.index)
-            self.sm_max = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
-            names = {nv.nvmlClocksEventReasonHwSlowdown: "hw_slowdown",
-                     nv.nvmlClocksEventReasonHwThermalSlowdown: "hw_thermal_slowdown",
-                     nv.nvmlClocksEventReasonSwThermalSlowdown: "sw_thermal_slowdown",
-                     nv.nvmlClocksEventReasonSwPowerCap: "sw_power_cap",
-                     nv.nvmlClocksEventReasonHwPowerBrakeSlowdown: "hw_power_brake"}
-            while not self._stop.is_set():
-                self.samples.append(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
-                r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
-                for bit, nm in names.items():
-                    if r & bit:
-                        self.reasons.add(nm)
-                time.sleep(self.period)
-            nv.nvmlShutdown()
+            self._nv = nv
+            self._h = nv.nvmlDeviceGetHandleByIndex(index)
+            self.sm_max = nv.nvmlDeviceGetMaxClockInfo(self._h, nv.NVML_CLOCK_SM)
+            self._bits = {getattr(nv, "nvmlClocksEventReason" + k): v for k, v in self.NAMES.items()}
         except Exception as exc:  # pragma: no cover - depends on the box
             self.err = repr(exc)
 
+    def _sample(self):
+        nv = self._nv
+        self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+        r = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+        for bit, nm in self._bits.items():
+            if r & bit:
+                self.reasons.add(nm)
+
+    def _run(self):
+        try:
+            while not self._stop.wait(self.period):
+                self._sample()
+        except Exception as exc:  # pragma: no cover
+            self.err = repr(exc)
+
     def start(self):
+        if self._nv is None:
+            return
+        self._sample()
         self._thr = threading.Thread(target=self._run, daemon=True)
         self._thr.start()
 
@@ -94,6 +106,11 @@ class ClockSampler:
         self._stop.set()
         if self._thr is not None:
             self._thr.join(timeout=5)
+        if self._nv is not None:
+            try:
+                self._sample()
+            except Exception as exc:  # pragma: no cover
+                self.err = repr(exc)
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": self.sm_max,
                     "reasons": [self.err or "no samples"]}
@@ -337,11 +354,17 @@ def run_ours(args, rank, world, local_rank):
                       "vs_cufft": round(cf / on, 4)})
     step_flops = sum(flops(c["n"], c["b"]) for c in cases) * world
     achieved = tot_bytes / tot_on / 1e6
+    # DRAM bytes per launch of these kernels from the committed ncu launch
+    # list (tools/launch_summary.py), averaged over the sweep's launches like
+    # `achieved` (algorithmic: 2 GiB per launch)
     traffic = None
-    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    tpath = os.path.join(ROOT, "profiles", "traffic_r01.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get("bytes_per_launch_sweep_total")
+            by_n = json.load(open(tpath))["dram_bytes_per_launch_by_n"]
+            vals = [by_n[str(c["n"])] for c in cases if str(c["n"]) in by_n]
+            if len(vals) == len(cases):
+                traffic = round(sum(vals) / len(vals))
         except Exception:
             traffic = None
     cpu = None
@@ -372,7 +395,7 @@ def run_ours(args, rank, world, local_rank):
         "vs_cufft_abft_off": round(tot_cufft / tot_off, 4),
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / hbm, 4),
-                     "traffic": traffic,
+                     "traffic": traffic, "traffic_algorithmic": 2 * BATCH_BYTES,
                      "kernel": "fft_single_kernel<float, N, ..., ABFT_WANG> (sweep aggregate: "
                                "algorithmic 2*N*8 B per signal / summed event time)"},
         "cpu_baseline": cpu,
