@@ -24,6 +24,12 @@ def main():
         per[r[ix["ID"]]]["name"] = r[ix["Kernel Name"]]
         val = float(r[ix["Metric Value"]].replace(",", ""))
         per[r[ix["ID"]]][r[ix["Metric Name"]]] = val
+    # full-batch launches only for the traffic figure (the e2e leg of the
+    # bench launches the same kernels on 32 MiB chunks)
+    full = collections.defaultdict(list)
+    for d in per.values():
+        full[re.sub(r"\(.*", "", d["name"])].append(
+            d.get("dram__bytes_read.sum", 0.0) + d.get("dram__bytes_write.sum", 0.0))
     agg = collections.OrderedDict()
     for lid, d in per.items():
         name = re.sub(r"\(.*", "", d["name"])
@@ -41,7 +47,8 @@ def main():
                      f"{100 * a['t'] / tot:.1f} % | {mean_b:.4g} |")
         m = re.search(r"fft_single_kernel<float, (\d+), \d+, \d+, 1,", name)
         if m:
-            traffic[m.group(1)] = mean_b
+            big = [b for b in full[name] if b >= 0.5 * max(full[name])]
+            traffic[m.group(1)] = sum(big) / len(big)
     open(md_out, "w").write("\n".join(lines) + "\n")
     json.dump({"dram_bytes_per_launch_by_n": traffic, "source": src}, open(js_out, "w"), indent=1)
     print("\n".join(lines[:25]))
