@@ -11,7 +11,7 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtfft.so")
+LIB_PATH = os.environ.get("TFFT_LIB_PATH") or os.path.join(_HERE, "libtfft.so")  # override: experiments only
 
 TFFT_OK, TFFT_EINVAL, TFFT_ECUDA, TFFT_ENOMEM, TFFT_EUNSUPPORTED, TFFT_EIO = 0, 1, 3, 4, 5, 6
 FP32, FP64 = 0, 1

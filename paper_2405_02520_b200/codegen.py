@@ -181,7 +181,7 @@ def single_configs(all_candidates=True):
                 st = n + 1 if c["stage"] in (1, 3) else 0
                 ib = s * n if c["stage"] in (2, 3) else 0  # TMA prefetch buffer
                 smem = ((ib + s * max(ex, st)) * ELEM_BYTES[prec]
-                        + 5 * (threads // 32 + 1) * (ELEM_BYTES[prec] // 2))
+                        + 10 * (threads // 32 + 1) * (ELEM_BYTES[prec] // 2))  # 5 sums per warp, x2 parity
                 out.append(dict(prec=prec, logn=logn, n=n, e=e, radices=radices, threads=threads,
                                 ps=ps, smem=smem, tps=tps, minb=c["minb"], stage=c["stage"],
                                 variant=vi, chosen=vi == chosen))

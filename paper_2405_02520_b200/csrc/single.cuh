@@ -18,6 +18,13 @@
 namespace tfft {
 
 enum { AT_NONE = 0, AT_INPUT = 1, AT_PRESCALE = 2, AT_OUTPUT = 3 };
+
+// Cost-attribution builds only (tools/ablate.py): drop parts of the fused
+// ABFT to time them. 1: cross-thread reduction, 2: c_in MACs, 4: l1 bound,
+// 8: c_out class sums. Never set in the product build.
+#ifndef TFFT_ABLATE
+#define TFFT_ABLATE 0
+#endif
 enum { ABFT_OFF = 0, ABFT_WANG = 1, ABFT_TABLE = 2 };
 
 template <class T> struct KeyT;
@@ -142,6 +149,22 @@ __device__ __forceinline__ void sig_sum(T (&val)[K], T* scratch, int t) {
     }
 }
 
+// TPS > 32: warp-level partial sums of K values, written by lane 0 of each
+// warp to `slot` (K per warp) with no barrier; the cross-warp sum and the
+// decision are deferred until after the next tile's first barrier.
+template <int K, class T>
+__device__ __forceinline__ void warp_partials(T (&val)[K], T* slot) {
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+#pragma unroll
+        for (int i = 0; i < K; ++i) val[i] = fadd(val[i], shfl_xor(val[i], off));
+    }
+    if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+        for (int i = 0; i < K; ++i) slot[(threadIdx.x >> 5) * K + i] = val[i];
+    }
+}
+
 // Smem slice length of one signal: the Stockham exchange buffer and/or the
 // staging buffer of coalesced I/O (stride N+1 keeps per-thread rows off the
 // same banks).
@@ -236,6 +259,59 @@ fft_single_kernel(const SingleArgs<T> a) {
         __syncthreads();
         if (threadIdx.x == 0 && blockIdx.x < tiles) prefetch(blockIdx.x);
     }
+    // Detection decision of one signal from its five reduced sums and the
+    // warp-aggregated append of flagged / recheck signals (rare). Every lane
+    // of the warp calls it (ballot); only `owner` lanes decide.
+    auto decide_signal = [&](const T (&sums)[5], long long bsig, bool owner) {
+        bool flagged = false, recheck = false;
+        T rel = T(0);
+        if (owner) {
+            T rel2;
+            abft_decide<T>(sums[0], sums[1], sums[2], sums[3], sums[4], a.delta, a.abs_floor, a.floor_coef,
+                           a.rel_out != nullptr, rel, rel2, flagged, recheck);
+            if (recheck) rel = T(-1);  // sentinel: the host recomputes it exactly
+            else my_max = my_max > rel2 ? my_max : rel2;  // squared; sqrt once per CTA
+            if (a.rel_out) a.rel_out[bsig] = rel;
+            flagged = flagged || recheck;
+        }
+        const unsigned ball = __ballot_sync(0xffffffffu, flagged);
+        if (ball) {
+            const int lane = threadIdx.x & 31;
+            int base = 0;
+            if (lane == __ffs(ball) - 1) base = atomicAdd(a.flag_count, __popc(ball));
+            base = __shfl_sync(0xffffffffu, base, __ffs(ball) - 1);
+            if (flagged) {
+                const long long slot = base + __popc(ball & ((1u << lane) - 1u));
+                if (slot < a.flag_cap) {
+                    a.flag_sig[slot] = a.sig_base + bsig;
+                    a.flag_rel[slot] = rel;
+                }
+            }
+        }
+    };
+    // TPS > 32: the previous tile's cross-warp sums, published through this
+    // tile's first barrier (double-buffered by tile parity)
+    constexpr bool DEFER = ABFT != ABFT_OFF && TPS > 32;
+    bool pend = false, pend_live = false;
+    long long pend_b = 0;
+    unsigned pend_par = 0;
+    auto finish_pending = [&]() {
+        T sums[5] = {T(0), T(0), T(0), T(0), T(0)};
+        const bool owner = t == 0 && pend_live;
+        if (owner) {
+            const T* pr = red + (size_t)pend_par * NW * 5;
+            const int warp = threadIdx.x >> 5;
+#pragma unroll
+            for (int i = 0; i < 5; ++i) {
+                T sacc = pr[warp * 5 + i];
+#pragma unroll
+                for (int w = 1; w < (TPS > 32 ? TPS / 32 : 1); ++w) sacc = fadd(sacc, pr[(warp + w) * 5 + i]);
+                sums[i] = sacc;
+            }
+        }
+        decide_signal(sums, pend_b, owner);
+        pend = false;
+    };
     unsigned iter = 0;
     for (long long tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++iter) {
         const long long b = tile * S + sl;
@@ -304,8 +380,8 @@ fft_single_kernel(const SingleArgs<T> a) {
         if constexpr (ABFT != ABFT_OFF) {
 #pragma unroll
             for (int m = 0; m < E; ++m) {
-                cin = cmac<T>(cin, v[m], ew[m]);
-                l1p = cadd<T>(l1p, cabs2<T>(v[m]));
+                if constexpr (!(TFFT_ABLATE & 2)) cin = cmac<T>(cin, v[m], ew[m]);
+                if constexpr (!(TFFT_ABLATE & 4)) l1p = cadd<T>(l1p, cabs2<T>(v[m]));
             }
         }
         int fw = a.f_where, fc = a.f_comp, fb = a.f_bit;
@@ -332,6 +408,9 @@ fft_single_kernel(const SingleArgs<T> a) {
         if (a.inverse) {
 #pragma unroll
             for (int m = 0; m < E; ++m) v[m] = swapri<T>(v[m]);
+        }
+        if constexpr (DEFER) {
+            if (pend) finish_pending();  // the exchanges above contain barriers
         }
         if (fault_here && fw == AT_PRESCALE) {
 #pragma unroll
@@ -367,7 +446,8 @@ fft_single_kernel(const SingleArgs<T> a) {
                 // e_k = w3^(k mod 3): sum per residue class, then 3 weights.
                 C<T> acc[3] = {mk<T>(T(0), T(0)), mk<T>(T(0), T(0)), mk<T>(T(0), T(0))};
 #pragma unroll
-                for (int m = 0; m < E; ++m) acc[m % 3] = cadd<T>(acc[m % 3], v[m]);
+                for (int m = 0; m < E; ++m)
+                    if constexpr (!(TFFT_ABLATE & 8)) acc[m % 3] = cadd<T>(acc[m % 3], v[m]);
                 constexpr int tau = TPS % 3;  // 1 or 2 (TPS is a power of two)
                 const int t0 = t % 3;
                 constexpr T hr = T(-0.5), hi = T(0.8660254037844386467637232);
@@ -387,33 +467,22 @@ fft_single_kernel(const SingleArgs<T> a) {
                 }
             }
             T sums[5] = {cin.x, cin.y, cout.x, cout.y, fadd(l1p.x, l1p.y)};
-            sig_sum<TPS>(sums, red, t);
-            bool flagged = false, recheck = false;
-            T rel = T(0);
-            if (t == 0 && live) {
-                T rel2;
-                abft_decide<T>(sums[0], sums[1], sums[2], sums[3], sums[4], a.delta, a.abs_floor, a.floor_coef,
-                               a.rel_out != nullptr, rel, rel2, flagged, recheck);
-                if (recheck) rel = T(-1);  // sentinel: the host recomputes it exactly
-                else my_max = my_max > rel2 ? my_max : rel2;  // squared; sqrt once per CTA
-                if (a.rel_out) a.rel_out[b] = rel;
-                flagged = flagged || recheck;
+            if constexpr (DEFER) {
+                if constexpr (!(TFFT_ABLATE & 1)) warp_partials<5>(sums, red + (size_t)(iter & 1) * NW * 5);
+                pend = true;
+                pend_live = live;
+                pend_b = b;
+                pend_par = iter & 1;
+            } else {
+                if constexpr (!(TFFT_ABLATE & 1)) sig_sum<TPS>(sums, red, t);
+                decide_signal(sums, b, t == 0 && live);
             }
-            // warp-aggregated append of flagged / recheck signals (rare)
-            const unsigned ball = __ballot_sync(0xffffffffu, flagged);
-            if (ball) {
-                const int lane = threadIdx.x & 31;
-                int base = 0;
-                if (lane == __ffs(ball) - 1) base = atomicAdd(a.flag_count, __popc(ball));
-                base = __shfl_sync(0xffffffffu, base, __ffs(ball) - 1);
-                if (flagged) {
-                    const long long slot = base + __popc(ball & ((1u << lane) - 1u));
-                    if (slot < a.flag_cap) {
-                        a.flag_sig[slot] = a.sig_base + b;
-                        a.flag_rel[slot] = rel;
-                    }
-                }
-            }
+        }
+    }
+    if constexpr (DEFER) {
+        if (pend) {
+            __syncthreads();
+            finish_pending();
         }
     }
     if constexpr (ABFT != ABFT_OFF) {
