@@ -300,11 +300,7 @@ fft_pass_kernel(const __grid_constant__ PassArgs<T> a) {
                 l1p = cadd<T>(l1p, cabs2<T>(v[m]));
             }
             T s[3] = {cin.x, cin.y, fadd(l1p.x, l1p.y)};
-            block_reduce<3>(s, red, THREADS / 32);
-            if (threadIdx.x == 0) {
-                T* p = a.part + (b * a.tiles_per_sig + tsig) * 3;
-                p[0] = s[0]; p[1] = s[1]; p[2] = s[2];
-            }
+            warp_partials<3>(s, red);  // summed by thread 0 after the tile's trailing barrier
         }
         if (fsig && fw == 1) {
 #pragma unroll
@@ -387,13 +383,23 @@ fft_pass_kernel(const __grid_constant__ PassArgs<T> a) {
                 }
             }
             T s[2] = {cout.x, cout.y};
-            block_reduce<2>(s, red, THREADS / 32);
+            warp_partials<2>(s, red);
+        }
+        __syncthreads();  // smem tile reused by the next iteration; warp partials visible
+        if constexpr (ABFT != ABFT_OFF && KIND != KIND_MID) {
+            // the tile's checksum partial (3 values in, 2 out), fixed warp order;
+            // `red` is rewritten only after the next tile's barriers
+            constexpr int K = KIND == KIND_FIRST ? 3 : 2;
             if (threadIdx.x == 0) {
-                T* p = a.part + (b * a.tiles_per_sig + tsig) * 2;
-                p[0] = s[0]; p[1] = s[1];
+                T* p = a.part + (b * a.tiles_per_sig + tsig) * K;
+#pragma unroll
+                for (int i = 0; i < K; ++i) {
+                    T acc = red[i];
+                    for (int w = 1; w < THREADS / 32; ++w) acc = fadd(acc, red[w * K + i]);
+                    p[i] = acc;
+                }
             }
         }
-        __syncthreads();  // smem tile reused by the next iteration
     }
 }
 
