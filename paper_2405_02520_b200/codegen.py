@@ -54,13 +54,17 @@ SINGLE_CANDIDATES = {
                    (16, (16, 16, 4), 256, 2, 2)),
         11: _cands((16, (16, 16, 8), 256, 2, 0), (16, (16, 16, 8), 256, 3, 0),
                    (8, (8, 8, 8, 4), 256, 3, 0), (16, (16, 16, 8), 512, 1, 0),
-                   (16, (16, 16, 8), 256, 3, 2), (16, (16, 16, 8), 256, 2, 2)),
+                   (16, (16, 16, 8), 256, 3, 2), (16, (16, 16, 8), 256, 2, 2),
+                   (16, (16, 16, 8), 256, 2, 4)),
         12: _cands((16, (16, 16, 16), 256, 2, 0), (16, (16, 16, 16), 256, 3, 0),
                    (8, (8, 8, 8, 8), 512, 2, 0), (16, (16, 16, 16), 512, 1, 0),
-                   (16, (16, 16, 16), 256, 3, 2), (16, (16, 16, 16), 256, 2, 2)),
+                   (16, (16, 16, 16), 256, 3, 2), (16, (16, 16, 16), 256, 2, 2),
+                   (16, (16, 16, 16), 256, 2, 4)),
         13: _cands((16, (16, 16, 16, 2), 512, 2, 0), (32, (32, 16, 16), 256, 1, 0),
                    (16, (16, 16, 16, 2), 512, 1, 0), (8, (8, 8, 8, 8, 2), 1024, 1, 0),
-                   (16, (16, 16, 16, 2), 512, 2, 2), (16, (16, 16, 16, 2), 512, 1, 2)),
+                   (16, (16, 16, 16, 2), 512, 2, 2), (16, (16, 16, 16, 2), 512, 1, 2),
+                   (16, (16, 16, 16, 2), 512, 2, 1), (16, (16, 16, 16, 2), 512, 2, 4),
+                   (16, (16, 16, 16, 2), 512, 1, 4)),
     },
     "fp64": {
         1: _cands((2, (2,), 256, 1, 1), (2, (2,), 256, 1, 0), (2, (2,), 256, 1, 3)),
@@ -82,17 +86,20 @@ SINGLE_CANDIDATES = {
         10: _cands((16, (16, 16, 4), 256, 1, 0), (8, (8, 8, 8, 2), 256, 1, 0),
                    (16, (16, 16, 4), 256, 2, 0), (16, (16, 16, 4), 256, 2, 2)),
         11: _cands((16, (16, 16, 8), 256, 1, 0), (16, (16, 16, 8), 256, 2, 0),
-                   (8, (8, 8, 8, 4), 256, 2, 0), (16, (16, 16, 8), 256, 2, 2)),
+                   (8, (8, 8, 8, 4), 256, 2, 0), (16, (16, 16, 8), 256, 2, 2),
+                   (8, (8, 8, 8, 4), 256, 2, 4)),
         12: _cands((16, (16, 16, 16), 256, 1, 0), (16, (16, 16, 16), 512, 1, 0),
-                   (8, (8, 8, 8, 8), 512, 1, 0), (16, (16, 16, 16), 256, 1, 2)),
-        13: _cands((16, (16, 16, 16, 2), 512, 1, 0), (8, (8, 8, 8, 8, 2), 1024, 1, 0)),
+                   (8, (8, 8, 8, 8), 512, 1, 0), (16, (16, 16, 16), 256, 1, 2),
+                   (16, (16, 16, 16), 256, 1, 4), (8, (8, 8, 8, 8), 512, 1, 4)),
+        13: _cands((16, (16, 16, 16, 2), 512, 1, 0), (8, (8, 8, 8, 8, 2), 1024, 1, 0),
+                   (16, (16, 16, 16, 2), 512, 1, 4), (8, (8, 8, 8, 8, 2), 1024, 1, 4)),
     },
 }
 # tuned winners (index into SINGLE_CANDIDATES[prec][logn]); missing -> 0.
 # Source: tools/tune.py on a B200, ABFT on, 1 GiB batches (profiles/tune_r01.json).
 SINGLE_CHOICE = {
-    "fp32": {1: 1, 2: 1, 3: 4, 4: 5, 5: 5, 6: 1, 7: 0, 8: 4, 9: 0, 10: 1, 11: 5, 12: 5, 13: 0},
-    "fp64": {1: 1, 2: 2, 3: 3, 4: 4, 5: 4, 6: 4, 7: 0, 8: 2, 9: 1, 10: 2, 11: 1, 12: 3, 13: 0},
+    "fp32": {1: 1, 2: 1, 3: 4, 4: 5, 5: 5, 6: 1, 7: 0, 8: 4, 9: 0, 10: 1, 11: 6, 12: 5, 13: 0},
+    "fp64": {1: 1, 2: 2, 3: 3, 4: 4, 5: 4, 6: 4, 7: 0, 8: 2, 9: 1, 10: 2, 11: 1, 12: 3, 13: 2},
 }
 ELEM_BYTES = {"fp32": 8, "fp64": 16}
 CTYPE = {"fp32": "float", "fp64": "double"}
@@ -178,7 +185,7 @@ def single_configs(all_candidates=True):
                 ps, _ = choose_padding(n, e, radices, prec)
                 s = threads // tps
                 ex = (n + (n >> ps) + 1 if ps else n) if len(radices) > 1 else 0
-                st = n + 1 if c["stage"] in (1, 3) else 0
+                st = n + 1 if c["stage"] in (1, 3) else (n if c["stage"] == 4 else 0)
                 ib = s * n if c["stage"] in (2, 3) else 0  # TMA prefetch buffer
                 smem = ((ib + s * max(ex, st)) * ELEM_BYTES[prec]
                         + 10 * (threads // 32 + 1) * (ELEM_BYTES[prec] // 2))  # 5 sums per warp, x2 parity

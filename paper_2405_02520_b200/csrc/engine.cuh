@@ -48,6 +48,7 @@ struct SliceMem {
     __device__ __forceinline__ void sync() const {
         if constexpr (TPS <= 32) __syncwarp(); else __syncthreads();
     }
+    __device__ __forceinline__ void after_last_exchange() const {}
 };
 // U transforms interleaved: element i of transform u at pad(i)*U + u.
 template <class T, int U, int PS>
@@ -57,6 +58,7 @@ struct TileMem {
     __device__ __forceinline__ void put(int i, C<T> v) const { base[padidx<PS>(i) * U + u] = v; }
     __device__ __forceinline__ C<T> get(int i) const { return base[padidx<PS>(i) * U + u]; }
     __device__ __forceinline__ void sync() const { __syncthreads(); }
+    __device__ __forceinline__ void after_last_exchange() const {}
 };
 
 template <class T, int L, int E, class Radices>
@@ -137,6 +139,7 @@ struct Engine {
 #pragma unroll
             for (int m = 0; m < E; ++m) v[m] = mem.get(t + m * TPS);
             mem.sync();
+            if constexpr (sizeof...(Rest) == 1) mem.after_last_exchange();
             passes<Ns * R>(v, mem, t, tw, RList<Rest...>{});
         }
     }

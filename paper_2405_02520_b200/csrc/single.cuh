@@ -168,11 +168,20 @@ __device__ __forceinline__ void warp_partials(T (&val)[K], T* slot) {
 // Smem slice length of one signal: the Stockham exchange buffer and/or the
 // staging buffer of coalesced I/O (stride N+1 keeps per-thread rows off the
 // same banks).
-template <int N, int PS, bool MULTIPASS, bool STAGE>
+template <int N, int PS, bool MULTIPASS, bool STAGE, bool INPLACE = false>
 struct SliceLen {
     static constexpr int ex = MULTIPASS ? SmemLen<N, PS>::v : 0;
-    static constexpr int st = STAGE ? N + 1 : 0;
+    static constexpr int st = STAGE ? N + 1 : (INPLACE ? N : 0);
     static constexpr int v = ex > st ? ex : st;
+};
+
+// Engine memory policy of the in-place prefetch (STAGE 4): the padded
+// exchange slices, plus a hook the engine calls once the last exchange has
+// been read back, when the buffer is free to receive the next tile.
+template <class T, int TPS, int PS, class Hook>
+struct SliceMemHook : SliceMem<T, TPS, PS> {
+    Hook hook;
+    __device__ __forceinline__ void after_last_exchange() const { hook(); }
 };
 
 // CTA-cooperative, fully coalesced vector copies between HBM and the staging
@@ -228,10 +237,16 @@ fft_single_kernel(const SingleArgs<T> a) {
     // + mbarrier) while the current tile computes.
     // 3: both — TMA prefetch of the next contiguous chunk, then an on-chip
     // reshuffle into the padded staging slices (short signals).
+    // 4: in-place TMA prefetch — the next tile lands in the exchange buffer
+    // itself (linear layout) once the last exchange of the current tile has
+    // been read, so prefetching costs no extra shared memory (two CTAs/SM at
+    // N = 8192).
     constexpr bool STG = STAGE == 1 || STAGE == 3;
     constexpr bool PF = STAGE == 2 || STAGE == 3;
+    constexpr bool PFI = STAGE == 4;
+    static_assert(!PFI || TPS > 32, "in-place prefetch needs CTA-wide exchange barriers");
     constexpr bool MULTIPASS = RCount<Radices>::v > 1;
-    constexpr int SL = SliceLen<N, PS, MULTIPASS, STG>::v;
+    constexpr int SL = SliceLen<N, PS, MULTIPASS, STG, PFI>::v;
     constexpr int NW = THREADS / 32 > 0 ? THREADS / 32 : 1;
 
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -248,13 +263,14 @@ fft_single_kernel(const SingleArgs<T> a) {
     if (threadIdx.x == 0) cta_max = 0;
 
     const long long tiles = (a.batch + S - 1) / S;
+    C<T>* const pf_dst = PFI ? sm_all : ib;
     auto prefetch = [&](long long tl) {  // thread 0 only
         const long long nsig = (a.batch - tl * S) < S ? (a.batch - tl * S) : S;
         const unsigned bytes = (unsigned)(nsig * N * sizeof(C<T>));
         mbar_expect_tx(&in_bar, bytes);
-        bulk_g2s(ib, a.in + tl * S * N, bytes, &in_bar);
+        bulk_g2s(pf_dst, a.in + tl * S * N, bytes, &in_bar);
     };
-    if constexpr (PF) {
+    if constexpr (PF || PFI) {
         if (threadIdx.x == 0) mbar_init(&in_bar, 1);
         __syncthreads();
         if (threadIdx.x == 0 && blockIdx.x < tiles) prefetch(blockIdx.x);
@@ -348,6 +364,17 @@ fft_single_kernel(const SingleArgs<T> a) {
 #pragma unroll
             for (int m = 0; m < E; ++m) v[m] = live ? sm[t + m * TPS] : mk<T>(T(0), T(0));
             __syncthreads();
+        } else if constexpr (PFI) {
+            mbar_wait(&in_bar, iter & 1);
+#pragma unroll
+            for (int m = 0; m < E; ++m) v[m] = live ? sm_all[sl * N + t + m * TPS] : mk<T>(T(0), T(0));
+            __syncthreads();  // linear tile consumed; the exchanges below reuse the buffer
+            if constexpr (!MULTIPASS) {
+                if (threadIdx.x == 0 && tile + gridDim.x < tiles) {
+                    fence_proxy_async();
+                    prefetch(tile + gridDim.x);
+                }
+            }
         } else if constexpr (PF) {
             mbar_wait(&in_bar, iter & 1);
 #pragma unroll
@@ -404,7 +431,18 @@ fft_single_kernel(const SingleArgs<T> a) {
 #pragma unroll
             for (int m = 0; m < E; ++m) v[m] = swapri<T>(v[m]);
         }
-        Eng::run(v, SliceMem<T, TPS, PS>{sm}, t, a.tw);
+        if constexpr (PFI && MULTIPASS) {
+            // refill the buffer as soon as the last exchange has been read
+            auto refill = [&]() {
+                if (threadIdx.x == 0 && tile + gridDim.x < tiles) {
+                    fence_proxy_async();
+                    prefetch(tile + gridDim.x);
+                }
+            };
+            Eng::run(v, SliceMemHook<T, TPS, PS, decltype(refill)>{{sm}, refill}, t, a.tw);
+        } else {
+            Eng::run(v, SliceMem<T, TPS, PS>{sm}, t, a.tw);
+        }
         if (a.inverse) {
 #pragma unroll
             for (int m = 0; m < E; ++m) v[m] = swapri<T>(v[m]);
