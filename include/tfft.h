@@ -154,6 +154,15 @@ int tfft_run_campaign(tfft_plan *plan, const void *in, void *out, int64_t runs,
                       int inverse, double *run_max_rel, int32_t *run_fired,
                       tfft_report *report, void *stream);
 
+/* Checksum granularity of the protected calls on this plan, for the paper's
+ * scheme comparison (TurboFFT one-sided vs thread-level vs threadblock-level;
+ * not a reference interface): 0 = threadblock-level two-sided checksums per
+ * signal (default, the reference's decisions), 1 = thread-level: every radix
+ * tile verified by the thread computing it (Wang encoding per tile; flags
+ * are then per-tile discrepancies, not the reference's). Level 1 is built for
+ * n <= 2^13 with the Wang encoding (values == NULL). */
+int tfft_set_check_level(tfft_plan *plan, int level);
+
 /* The two halves of tfft_run_protected, for callers that queue several
  * protected transforms before reading their reports (one in-flight protected
  * call per plan): _launch enqueues the fused transform and the tiny

@@ -207,9 +207,9 @@ def _emit_single(prec, cfgs, part, table=False):
     for c in cfgs:
         rl = ", ".join(str(r) for r in c["radices"])
         fns = []
-        for abft in (0, 1, 2):
-            if abft == 2 and not c["chosen"]:
-                fns.append("nullptr")  # table encodings only on the chosen config
+        for abft in (0, 1, 2, 3):
+            if abft >= 2 and not c["chosen"]:
+                fns.append("nullptr")  # table / thread-level checks only on the chosen config
                 continue
             fns.append(f"(const void*)&fft_single_kernel<{t}, {c['n']}, {c['e']}, {c['ps']}, "
                        f"{abft}, {c['threads']}, {c['minb']}, {c['stage']}, RList<{rl}>>")
@@ -402,9 +402,46 @@ def _write(path, text):
             f.write(text)
 
 
+def wang_etw_header():
+    """Constants of the thread-level check (ABFT_THREAD): e^T W of the Wang
+    weights e_k = w3^(k mod 3) for one radix-R tile, etw_R[r] = sum_k e_k
+    w_R^(r k), rounded once from 50-digit arithmetic."""
+    try:
+        import mpmath as mp
+        mp.mp.dps = 50
+
+        def etw(R, r):
+            z = sum(mp.expjpi(-mp.mpf(2) * (k % 3) / 3) * mp.expjpi(-mp.mpf(2) * r * k / R) for k in range(R))
+            return float(mp.re(z)), float(mp.im(z))
+    except ImportError:  # pragma: no cover - long double fallback
+        import numpy as np
+
+        def etw(R, r):
+            k = np.arange(R, dtype=np.longdouble)
+            ang = -2 * np.pi * ((k % 3) / 3 + r * k / R)
+            return float(np.cos(ang).sum()), float(np.sin(ang).sum())
+    lines = ["// GENERATED by paper_2405_02520_b200/codegen.py (wang_etw_header) — do not edit.",
+             "// Thread-level ABFT: e^T W of the Wang weights for one radix-R tile,",
+             "// etw_R[r] = sum_k w3^(k mod 3) w_R^(r k), rounded once from 50 digits.",
+             "// Constexpr lookups: with unrolled (compile-time) r they fold to immediates.",
+             "#pragma once", "namespace tfft {"]
+    for part, name in ((0, "re"), (1, "im")):
+        lines.append(f"__host__ __device__ constexpr double wang_etw_{name}(int R, int r) {{")
+        for R in (2, 4, 8, 16, 32):
+            vals = [etw(R, r)[part] for r in range(R)]
+            lines.append(f"    constexpr double t{R}[{R}] = {{{', '.join(repr(v) for v in vals)}}};")
+        lines.append("    return R == 2 ? t2[r] : R == 4 ? t4[r] : R == 8 ? t8[r] : R == 16 ? t16[r] : t32[r];")
+        lines.append("}")
+    lines.append("}  // namespace tfft")
+    return "\n".join(lines) + "\n"
+
+
 def generate(verbose=False):
     cfgs = single_configs()
     written = []
+    path = os.path.join(CSRC, "wang_etw.cuh")
+    _write(path, wang_etw_header())
+    written.append(path)
     for old in ("gen_single_fp32.cu", "gen_single_fp64.cu"):
         if os.path.exists(os.path.join(CSRC, old)):
             os.remove(os.path.join(CSRC, old))

@@ -149,6 +149,21 @@ struct FixJob {
     int pad;
 };
 
+// s0 of K flagged groups in one launch (grid.y = group): s0[k] = sum over
+// the group's bs signals, sequential in b like group_sums_kernel.
+template <class T>
+__global__ void group_sums_jobs_kernel(const C<T>* __restrict__ in, long long bs, long long n,
+                                       const FixJob* __restrict__ jobs, C<T>* __restrict__ s0) {
+    const C<T>* xg = in + jobs[blockIdx.y].first * n;
+    C<T>* dst = s0 + (long long)blockIdx.y * n;
+    for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n;
+         k += (long long)gridDim.x * blockDim.x) {
+        C<T> a = xg[k];
+        for (long long b = 1; b < bs; ++b) a = cadd<T>(a, xg[b * n + k]);
+        dst[k] = a;
+    }
+}
+
 // Online correction of K flagged groups, one CTA per group:
 //   fixed = W s0 - sum_{b != f} y_b  (pipeline.py:180-185),
 //   then re-verify the rebuilt signal against its input-side checksum and

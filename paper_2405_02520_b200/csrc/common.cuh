@@ -297,6 +297,10 @@ __device__ __forceinline__ float mag_fast(float2 z) {
     asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(s));
     return r;
 }
+template <class T> __device__ __forceinline__ T nanmax(T a, T b) {
+    return (a != a) ? a : ((b != b) ? b : (a > b ? a : b));
+}
+
 // (|re|, |im|): per-element term of the l1 upper bound sum(|re| + |im|)
 template <class T> __device__ __forceinline__ C<T> cabs2(C<T> z) { return mk<T>(fabs(z.x), fabs(z.y)); }
 

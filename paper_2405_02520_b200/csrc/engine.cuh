@@ -18,6 +18,7 @@
 // U lanes of a row hit consecutive banks (multi-pass tiles).
 #pragma once
 #include "common.cuh"
+#include "wang_etw.cuh"
 
 namespace tfft {
 
@@ -61,6 +62,53 @@ struct TileMem {
     __device__ __forceinline__ void after_last_exchange() const {}
 };
 
+// Per-tile check policy of the engine: `pre` sees a radix tile before its
+// DFT, `post` after it. NoCheck compiles away; TileCheck is the thread-level
+// two-sided ABFT of the paper's scheme comparison (each thread verifies the
+// radix-R DFTs it computes with the Wang encoding: c_in = a . e^T W_R before,
+// c_out = A . e after), keeping the worst squared relative discrepancy.
+struct NoCheck {
+    template <int R, class T> __device__ __forceinline__ C<T> pre(const C<T>*) { return C<T>{}; }
+    template <int R, class T> __device__ __forceinline__ void post(const C<T>*, C<T>) const {}
+};
+template <class T>
+struct TileCheck {
+    // max |c_in - c_out|^2 / max(|c_in|, abs_floor, TILE_FLOOR * l1_tile)^2.
+    // A radix tile's checksums carry rounding noise ~eps * sum|a|, so the
+    // relative test needs a tile-scale floor (1e-2 fp32, 1e-6 fp64: noise /
+    // floor stays ~1e-4 / 1e-9 below the default deltas).
+    static constexpr T TILE_FLOOR = sizeof(T) == 4 ? T(1e-2) : T(1e-6);
+    T worst = T(0);
+    T floor2 = T(0);
+    T tile_l1 = T(0);
+    template <int R, class U> __device__ __forceinline__ C<T> pre(const C<T>* a) {
+        C<T> c = mk<T>(T(0), T(0));
+        C<T> l = mk<T>(T(0), T(0));
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            c = cmac<T>(c, a[r], mk<T>((T)wang_etw_re(R, r), (T)wang_etw_im(R, r)));
+            l = cadd<T>(l, cabs2<T>(a[r]));
+        }
+        tile_l1 = fmul(TILE_FLOOR, fadd(l.x, l.y));
+        return c;
+    }
+    template <int R, class U> __device__ __forceinline__ void post(const C<T>* A, C<T> cin) {
+        C<T> acc[3] = {mk<T>(T(0), T(0)), mk<T>(T(0), T(0)), mk<T>(T(0), T(0))};
+#pragma unroll
+        for (int k = 0; k < R; ++k) acc[k % 3] = cadd<T>(acc[k % 3], A[k]);
+        constexpr T hr = T(-0.5), hi = T(0.8660254037844386467637232);
+        C<T> cout = acc[0];
+        if (R > 1) cout = cadd<T>(cout, cmul<T>(acc[1], mk<T>(hr, -hi)));
+        if (R > 2) cout = cadd<T>(cout, cmul<T>(acc[2], mk<T>(hr, hi)));
+        const T dx = fsub(cin.x, cout.x), dy = fsub(cin.y, cout.y);
+        const T raw2 = ffma(dx, dx, fmul(dy, dy));
+        const T fl = tile_l1;
+        const T den2 = nanmax<T>(nanmax<T>(ffma(cin.x, cin.x, fmul(cin.y, cin.y)), floor2), fmul(fl, fl));
+        const T q = raw2 / den2;
+        worst = (q != q) ? T(INFINITY) : (q > worst ? q : worst);
+    }
+};
+
 template <class T, int L, int E, class Radices>
 struct Engine {
     static constexpr int TPS = L / E;
@@ -72,7 +120,13 @@ struct Engine {
     template <class Mem>
     static __device__ __forceinline__ void run(C<T> (&v)[E], const Mem& mem, int t,
                                                const C<T>* __restrict__ tw) {
-        passes<1>(v, mem, t, tw, Radices{});
+        NoCheck chk;
+        passes<1>(v, mem, t, tw, chk, Radices{});
+    }
+    template <class Mem, class Check>
+    static __device__ __forceinline__ void run(C<T> (&v)[E], const Mem& mem, int t,
+                                               const C<T>* __restrict__ tw, Check& chk) {
+        passes<1>(v, mem, t, tw, chk, Radices{});
     }
 
   private:
@@ -110,9 +164,9 @@ struct Engine {
         }
     }
 
-    template <int Ns, class Mem, int R, int... Rest>
+    template <int Ns, class Mem, class Check, int R, int... Rest>
     static __device__ __forceinline__ void passes(C<T> (&v)[E], const Mem& mem, int t,
-                                                  const C<T>* __restrict__ tw,
+                                                  const C<T>* __restrict__ tw, Check& chk,
                                                   RList<R, Rest...>) {
         static_assert(E % R == 0, "radix must divide elements per thread");
         constexpr int SUB = E / R;
@@ -123,7 +177,9 @@ struct Engine {
             C<T> a[R];
 #pragma unroll
             for (int r = 0; r < R; ++r) a[r] = v[q + r * SUB];
+            const C<T> ci = chk.template pre<R, T>(a);
             Dft<T, R>::run(a);
+            chk.template post<R, T>(a, ci);
 #pragma unroll
             for (int r = 0; r < R; ++r) v[q + r * SUB] = a[r];
         }
@@ -140,12 +196,12 @@ struct Engine {
             for (int m = 0; m < E; ++m) v[m] = mem.get(t + m * TPS);
             mem.sync();
             if constexpr (sizeof...(Rest) == 1) mem.after_last_exchange();
-            passes<Ns * R>(v, mem, t, tw, RList<Rest...>{});
+            passes<Ns * R>(v, mem, t, tw, chk, RList<Rest...>{});
         }
     }
-    template <int Ns, class Mem>
+    template <int Ns, class Mem, class Check>
     static __device__ __forceinline__ void passes(C<T> (&)[E], const Mem&, int, const C<T>* __restrict__,
-                                                  RList<>) {}
+                                                  Check&, RList<>) {}
 };
 
 }  // namespace tfft

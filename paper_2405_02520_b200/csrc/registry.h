@@ -11,7 +11,7 @@ struct SingleEntry {
     int threads;     // CTA size
     int smem;        // dynamic shared memory bytes
     int tps;         // threads per signal
-    const void* fn[3];  // ABFT off / Wang / table (table only on the chosen variant)
+    const void* fn[4];  // ABFT off / Wang / table / thread-level (last two only on the chosen variant)
 };
 
 struct SingleTable {

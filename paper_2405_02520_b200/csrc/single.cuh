@@ -25,7 +25,10 @@ enum { AT_NONE = 0, AT_INPUT = 1, AT_PRESCALE = 2, AT_OUTPUT = 3 };
 #ifndef TFFT_ABLATE
 #define TFFT_ABLATE 0
 #endif
-enum { ABFT_OFF = 0, ABFT_WANG = 1, ABFT_TABLE = 2 };
+// ABFT_THREAD: the paper's thread-level scheme (scheme comparison only):
+// every radix tile is verified by its thread (engine TileCheck) instead of
+// the per-signal threadblock checksums.
+enum { ABFT_OFF = 0, ABFT_WANG = 1, ABFT_TABLE = 2, ABFT_THREAD = 3 };
 
 template <class T> struct KeyT;
 template <> struct KeyT<float>  { using type = unsigned int; };
@@ -66,9 +69,6 @@ struct SingleArgs {
     long long f_div;
 };
 
-template <class T> __device__ __forceinline__ T nanmax(T a, T b) {
-    return (a != a) ? a : ((b != b) ? b : (a > b ? a : b));
-}
 
 // Detection decision of one signal from its reduced checksums (reference
 // pipeline.py:104-121): rel = |c_in - c_out| / max(|c_in|, max(abs_floor,
@@ -307,7 +307,8 @@ fft_single_kernel(const SingleArgs<T> a) {
     };
     // TPS > 32: the previous tile's cross-warp sums, published through this
     // tile's first barrier (double-buffered by tile parity)
-    constexpr bool DEFER = ABFT != ABFT_OFF && TPS > 32;
+    constexpr bool TB = ABFT == ABFT_WANG || ABFT == ABFT_TABLE;  // threadblock-level checksums
+    constexpr bool DEFER = TB && TPS > 32;
     bool pend = false, pend_live = false;
     long long pend_b = 0;
     unsigned pend_par = 0;
@@ -338,8 +339,8 @@ fft_single_kernel(const SingleArgs<T> a) {
 
         // input-side ABFT row e^T W at this thread's positions (the same for
         // every tile: L1 hits), requested before the tile data is waited for
-        C<T> ew[ABFT != ABFT_OFF ? E : 1];
-        if constexpr (ABFT != ABFT_OFF) {
+        C<T> ew[TB ? E : 1];
+        if constexpr (TB) {
 #pragma unroll
             for (int m = 0; m < E; ++m) ew[m] = __ldg(a.etw + t + m * TPS);
         }
@@ -404,7 +405,7 @@ fft_single_kernel(const SingleArgs<T> a) {
         // ---- left-side input checksum on the pristine values
         C<T> cin = mk<T>(T(0), T(0));
         C<T> l1p = mk<T>(T(0), T(0));  // (sum |re|, sum |im|): the l1 upper bound
-        if constexpr (ABFT != ABFT_OFF) {
+        if constexpr (TB) {
 #pragma unroll
             for (int m = 0; m < E; ++m) {
                 if constexpr (!(TFFT_ABLATE & 2)) cin = cmac<T>(cin, v[m], ew[m]);
@@ -431,6 +432,9 @@ fft_single_kernel(const SingleArgs<T> a) {
 #pragma unroll
             for (int m = 0; m < E; ++m) v[m] = swapri<T>(v[m]);
         }
+        // thread-level scheme: each thread verifies its radix tiles
+        TileCheck<T> tchk;
+        tchk.floor2 = fmul(a.abs_floor, a.abs_floor);
         if constexpr (PFI && MULTIPASS) {
             // refill the buffer as soon as the last exchange has been read
             auto refill = [&]() {
@@ -439,9 +443,13 @@ fft_single_kernel(const SingleArgs<T> a) {
                     prefetch(tile + gridDim.x);
                 }
             };
-            Eng::run(v, SliceMemHook<T, TPS, PS, decltype(refill)>{{sm}, refill}, t, a.tw);
+            const SliceMemHook<T, TPS, PS, decltype(refill)> mem{{sm}, refill};
+            if constexpr (ABFT == ABFT_THREAD) Eng::run(v, mem, t, a.tw, tchk);
+            else Eng::run(v, mem, t, a.tw);
         } else {
-            Eng::run(v, SliceMem<T, TPS, PS>{sm}, t, a.tw);
+            const SliceMem<T, TPS, PS> mem{sm};
+            if constexpr (ABFT == ABFT_THREAD) Eng::run(v, mem, t, a.tw, tchk);
+            else Eng::run(v, mem, t, a.tw);
         }
         if (a.inverse) {
 #pragma unroll
@@ -478,7 +486,52 @@ fft_single_kernel(const SingleArgs<T> a) {
                 else dst[t + m * TPS] = v[m];
             }
         }
-        if constexpr (ABFT != ABFT_OFF) {
+        if constexpr (ABFT == ABFT_THREAD) {
+            // worst tile of the signal (max over its threads), one decision
+            T w = tchk.worst;
+            constexpr int W = TPS < 32 ? TPS : 32;
+#pragma unroll
+            for (int off = W / 2; off >= 1; off >>= 1) {
+                const T o = shfl_xor(w, off);
+                w = (o != o || o > w) ? o : w;
+            }
+            if constexpr (TPS > 32) {
+                if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = w;
+                __syncthreads();
+                if (t == 0) {
+                    for (int k = 1; k < TPS / 32; ++k) {
+                        const T o = red[(threadIdx.x >> 5) + k];
+                        w = (o != o || o > w) ? o : w;
+                    }
+                }
+                __syncthreads();
+            }
+            bool flagged = false;
+            T rel = T(0);
+            if (t == 0 && live) {
+                rel = (w != w) ? T(INFINITY) : sqrt(w);
+                if (!isfinite(rel)) rel = T(INFINITY);
+                flagged = rel > a.delta;
+                const T r2 = rel * rel;
+                my_max = my_max > r2 ? my_max : r2;
+                if (a.rel_out) a.rel_out[b] = rel;
+            }
+            const unsigned ball = __ballot_sync(0xffffffffu, flagged);
+            if (ball) {
+                const int lane = threadIdx.x & 31;
+                int base = 0;
+                if (lane == __ffs(ball) - 1) base = atomicAdd(a.flag_count, __popc(ball));
+                base = __shfl_sync(0xffffffffu, base, __ffs(ball) - 1);
+                if (flagged) {
+                    const long long slot = base + __popc(ball & ((1u << lane) - 1u));
+                    if (slot < a.flag_cap) {
+                        a.flag_sig[slot] = a.sig_base + b;
+                        a.flag_rel[slot] = rel;
+                    }
+                }
+            }
+        }
+        if constexpr (TB) {
             C<T> cout = mk<T>(T(0), T(0));
             if constexpr (ABFT == ABFT_WANG) {
                 // e_k = w3^(k mod 3): sum per residue class, then 3 weights.

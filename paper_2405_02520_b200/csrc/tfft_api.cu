@@ -175,6 +175,7 @@ struct tfft_plan {
     int64_t dims[3] = {0, 0, 0};
     int64_t bs = 1;
     int device = 0;
+    int check_level = 0;            // 0 threadblock checksums, 1 thread-level (scheme comparison)
     int logn = 0;
     int num_sms = 148;
     size_t esize = 8;               // bytes per complex element
@@ -465,7 +466,7 @@ int prepare_protected(tfft_plan* p, const void* in, void* out, int64_t batch, in
     rep->fault_fired = 0;
 
     L = base_launch(in, out, batch, inverse ? 1 : 0);
-    L.abft = prot ? (values ? ABFT_TABLE : ABFT_WANG) : ABFT_OFF;
+    L.abft = prot ? (values ? ABFT_TABLE : (p->check_level ? ABFT_THREAD : ABFT_WANG)) : ABFT_OFF;
     L.etw = etw;
     L.values = values;
     L.delta = delta;
@@ -887,7 +888,7 @@ int correct_groups(tfft_plan* p, const void* in, void* out, int scheme, const vo
         }
         return TFFT_OK;
     }
-    const int64_t chunk_max = std::max<int64_t>(1, std::min<int64_t>(256, (int64_t(1) << 28) / (n * (int64_t)p->esize)));
+    const int64_t chunk_max = std::max<int64_t>(1, std::min<int64_t>(4096, (int64_t(1) << 28) / (n * (int64_t)p->esize)));
     for (size_t c0 = 0; c0 < fix_groups.size(); c0 += chunk_max) {
         const int64_t K = std::min<int64_t>(chunk_max, fix_groups.size() - c0);
         rc = ensure_scratch(p, (size_t)3 * K * n * p->esize);
@@ -902,25 +903,25 @@ int correct_groups(tfft_plan* p, const void* in, void* out, int scheme, const vo
             p->jobs_cap = K;
         }
         std::vector<FixJob> jobs(K);
-        const int grid = (int)std::min<long long>((n + 255) / 256, 4LL * p->num_sms);
         for (int64_t k = 0; k < K; ++k) {
-            const int64_t g = fix_groups[c0 + k];
-            jobs[k].first = g * p->bs;
+            jobs[k].first = fix_groups[c0 + k] * p->bs;
             jobs[k].flagged = fix_sig[c0 + k];
             jobs[k].ok = 0;
-            const char* xg = (const char*)in + (size_t)g * p->bs * n * p->esize;
-            if (p->prec == TFFT_FP32)
-                group_sums_kernel<float><<<grid, 256, 0, st>>>((const float2*)xg, p->bs, n,
-                                                               (float2*)(s0 + k * n * p->esize), nullptr);
-            else
-                group_sums_kernel<double><<<grid, 256, 0, st>>>((const double2*)xg, p->bs, n,
-                                                                (double2*)(s0 + k * n * p->esize), nullptr);
         }
+        CU(cudaMemcpyAsync(p->d_jobs, jobs.data(), K * sizeof(FixJob), cudaMemcpyHostToDevice, st));
+        // all K group sums in one launch, then one batched FFT of them
+        const unsigned gx = (unsigned)std::max<long long>(1, std::min<long long>((n + 255) / 256,
+                                                                               (4LL * p->num_sms + K - 1) / K));
+        if (p->prec == TFFT_FP32)
+            group_sums_jobs_kernel<float><<<dim3(gx, (unsigned)K), 256, 0, st>>>((const float2*)in, p->bs, n,
+                                                                                p->d_jobs, (float2*)s0);
+        else
+            group_sums_jobs_kernel<double><<<dim3(gx, (unsigned)K), 256, 0, st>>>((const double2*)in, p->bs, n,
+                                                                                 p->d_jobs, (double2*)s0);
         CU(cudaGetLastError());
         Launch W = base_launch(s0, ws0, K, inverse ? 1 : 0);
         rc = launch_transform(p, W, st);
         if (rc) return rc;
-        CU(cudaMemcpyAsync(p->d_jobs, jobs.data(), K * sizeof(FixJob), cudaMemcpyHostToDevice, st));
         if (p->prec == TFFT_FP32)
             fix_groups_kernel<float><<<(unsigned)K, AUX_THREADS, 0, st>>>(
                 (const float2*)in, (float2*)out, n, p->bs, (const float2*)ws0, (float2*)fx,
@@ -1571,6 +1572,18 @@ int tfft_element_verify(int r, int64_t B, void* y, const void* row_in, const voi
     CU(cudaMemcpyAsync(result, d_res, 3 * sizeof(int), cudaMemcpyDeviceToHost, st));
     CU(cudaFreeAsync(d_res, st));
     CU(cudaStreamSynchronize(st));
+    return TFFT_OK;
+}
+
+}  // extern "C"
+
+extern "C" {
+
+int tfft_set_check_level(tfft_plan* p, int level) {
+    if (!p) return fail(TFFT_EINVAL, "null plan");
+    if (level != 0 && level != 1) return fail(TFFT_EINVAL, "check level must be 0 (threadblock) or 1 (thread)");
+    if (level == 1 && !p->single) return fail(TFFT_EUNSUPPORTED, "thread-level checks are built for n <= 2^13");
+    p->check_level = level;
     return TFFT_OK;
 }
 

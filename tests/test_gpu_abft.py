@@ -294,3 +294,35 @@ def test_floor_recheck_path_matches_oracle(n, prec, device_input):
         assert mine["discrepancy"] > 10 * delta and theirs["discrepancy"] > 10 * delta
         assert 0.2 < mine["discrepancy"] / theirs["discrepancy"] < 5
     assert rep.max_rel_discrepancy > 0 and math.isfinite(rep.max_rel_discrepancy)
+
+
+def test_thread_level_check_level():
+    """Check level 1 (the paper's thread-level scheme, scheme comparison
+    only): outputs bitwise equal to the unprotected transform, no false
+    alarms on clean data. It verifies each radix tile's DFT, so corruption of
+    the data between tiles (an "input" fault here) is outside its coverage —
+    while the default threadblock checksums catch and correct it."""
+    from paper_2405_02520_b200 import _lib
+    from paper_2405_02520_b200.fft_core.plan import native_plan
+    n, b = 1024, 64
+    x = random_batch(np.random.default_rng(4), (b, n), np.complex64)
+    plan = fit_group_size(make_plan(n, "fp32", batch=b), b)
+    tw = build_twiddles(plan)
+    ref, _, _ = run_protected(plan, tw, torch.from_numpy(x).cuda(), Scheme.NONE)
+    h = native_plan(plan, torch.cuda.current_device())
+    spec = FaultSpec(0, 9, 100, "re", 26, "input")  # finite (x 2^8): consistent inside every tile
+    _lib.check(_lib.load().tfft_set_check_level(h.handle, 1))
+    try:
+        y, rep, _ = run_protected(plan, tw, torch.from_numpy(x).cuda(), Scheme.TWO_SIDED_GROUP)
+        assert rep.flagged == [] and torch.equal(y, ref)
+        _, rep, _ = run_protected(plan, tw, torch.from_numpy(x).cuda(), Scheme.TWO_SIDED_GROUP,
+                                  injector=BitFlipInjector(spec))
+        assert rep.flagged == []
+    finally:
+        _lib.check(_lib.load().tfft_set_check_level(h.handle, 0))
+    y, rep, _ = run_protected(plan, tw, torch.from_numpy(x).cuda(), Scheme.TWO_SIDED_GROUP,
+                              injector=BitFlipInjector(spec))
+    assert [c["signal"] for c in rep.corrected] == [9] and rel_l2(y, ref) < 1e-6
+    with pytest.raises(NotImplementedError):
+        big = fit_group_size(make_plan(1 << 16, "fp32", batch=16), 16)
+        _lib.check(_lib.load().tfft_set_check_level(native_plan(big, torch.cuda.current_device()).handle, 1))

@@ -1,0 +1,122 @@
+"""The paper's scheme comparison on B200 (PAPER.md: one-sided vs
+thread-level vs threadblock-level ABFT; A100: 29 / 13.4 / 8.9 % overhead) and
+the online-correction overhead (C4: 2-3 % in the paper).
+
+Per size, 1 GiB batch, CUDA events, median of 7:
+- none: fused kernel without checksums;
+- threadblock: the default two-sided per-signal checksums (tfft check level 0);
+- thread: every radix tile verified by its thread (check level 1);
+- correction at a fault rate: tfft_run_campaign over runs = checksum groups,
+  one exponent-bit output fault in every `--every`-th group, two-sided
+  (rebuild from the group sum) vs one-sided (recompute), relative to the same
+  launch with no faults.
+Writes gpurun_out/schemes.json.
+"""
+import argparse
+import ctypes
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--cases", default="fp32:8,fp32:10,fp32:12,fp64:10")
+    ap.add_argument("--every", type=int, default=100)
+    ap.add_argument("--reps", type=int, default=7)
+    a = ap.parse_args()
+    import torch
+    from paper_2405_02520_b200 import _lib, make_plan
+    from paper_2405_02520_b200.abft import make_encoding
+    from paper_2405_02520_b200.fft_core import fit_group_size
+    from paper_2405_02520_b200.fft_core.plan import native_plan
+    lib = _lib.load()
+    sp = torch.cuda.current_stream().cuda_stream
+    out = []
+
+    def timed(fn):
+        ts = []
+        for i in range(a.reps + 2):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn()
+            e1.record()
+            torch.cuda.synchronize()
+            if i >= 2:
+                ts.append(e0.elapsed_time(e1))
+        return sorted(ts)[len(ts) // 2]
+
+    for case in a.cases.split(","):
+        prec, logn = case.split(":")
+        logn = int(logn)
+        n = 1 << logn
+        dt, es = (torch.complex64, 8) if prec == "fp32" else (torch.complex128, 16)
+        b = (1 << 30) // (es * n)
+        x = torch.randn(b * n, dtype=dt, device="cuda")
+        y = torch.empty_like(x)
+        plan = fit_group_size(make_plan(n, prec, batch=b), b)
+        h = native_plan(plan, 0)
+        row = make_encoding("wang", n).device_row(dt)
+        delta = 1e-4 if prec == "fp32" else 1e-9
+        rep = _lib.Report()
+
+        def run(scheme):
+            _lib.check(lib.tfft_run_protected(h.handle, x.data_ptr(), y.data_ptr(), b, _lib.SCHEME_CODE[scheme],
+                                              delta, 0.0, row.data_ptr(), None, None, 0, ctypes.byref(rep), sp))
+
+        r = {"prec": prec, "n": n, "batch": b, "bs": plan.bs}
+        r["ms_none"] = timed(lambda: run("none"))
+        _lib.check(lib.tfft_set_check_level(h.handle, 0))
+        r["ms_threadblock"] = timed(lambda: run("two_sided_group"))
+        _lib.check(lib.tfft_set_check_level(h.handle, 1))
+        r["ms_thread"] = timed(lambda: run("two_sided_group"))
+        r["thread_flagged_clean"] = int(rep.n_flagged)
+        _lib.check(lib.tfft_set_check_level(h.handle, 0))
+        # online correction: one output fault every `every` groups
+        runs = b // plan.bs
+        faults = (_lib.Fault * runs)()
+        nf = 0
+        for g in range(0, runs, a.every):
+            f = faults[g]
+            f.signal, f.element, f.where, f.stage, f.component, f.bit = 1 % plan.bs, 7, _lib.AT_OUTPUT, 0, 0, 30 if prec == "fp32" else 62
+            nf += 1
+        rmax = (ctypes.c_double * runs)()
+        for scheme in ("two_sided_group", "one_sided"):
+            def camp(fs):
+                _lib.check(lib.tfft_run_campaign(h.handle, x.data_ptr(), y.data_ptr(), runs, plan.bs,
+                                                 _lib.SCHEME_CODE[scheme], delta, 0.0, row.data_ptr(), None,
+                                                 fs, 0, rmax, None, ctypes.byref(rep), sp))
+            clean = timed(lambda: camp(None))
+            faulty = timed(lambda: camp(faults))
+            r[f"{scheme}_ms_clean"] = clean
+            r[f"{scheme}_ms_faults"] = faulty
+            r[f"{scheme}_corrected"] = int(rep.n_corrected)
+            r[f"{scheme}_correction_overhead_pct"] = round(100 * (faulty / clean - 1), 2)
+        # one fault per launch (the paper's online-correction setting)
+        one = _lib.Fault()
+        one.signal, one.element, one.where, one.stage, one.component = b // 2, 7, _lib.AT_OUTPUT, 0, 0
+        one.bit = 30 if prec == "fp32" else 62
+        for scheme in ("two_sided_group", "one_sided"):
+            def single(f):
+                _lib.check(lib.tfft_run_protected(h.handle, x.data_ptr(), y.data_ptr(), b, _lib.SCHEME_CODE[scheme],
+                                                  delta, 0.0, row.data_ptr(), None, f, 0, ctypes.byref(rep), sp))
+            clean = timed(lambda: single(None))
+            faulty = timed(lambda: single(ctypes.byref(one)))
+            r[f"{scheme}_one_fault_overhead_pct"] = round(100 * (faulty / clean - 1), 2)
+            r[f"{scheme}_one_fault_corrected"] = int(rep.n_corrected)
+        r["faults"] = nf
+        r["fault_rate"] = f"1 per {a.every} groups of {plan.bs}"
+        r["overhead_threadblock_pct"] = round(100 * (r["ms_threadblock"] / r["ms_none"] - 1), 2)
+        r["overhead_thread_pct"] = round(100 * (r["ms_thread"] / r["ms_none"] - 1), 2)
+        print(json.dumps(r), flush=True)
+        out.append(r)
+        del x, y
+    os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+    json.dump(out, open(os.path.join(ROOT, "gpurun_out", "schemes.json"), "w"), indent=1)
+
+
+if __name__ == "__main__":
+    main()
