@@ -98,8 +98,8 @@ SINGLE_CANDIDATES = {
 # tuned winners (index into SINGLE_CANDIDATES[prec][logn]); missing -> 0.
 # Source: tools/tune.py on a B200, ABFT on, 1 GiB batches (profiles/tune_r01.json).
 SINGLE_CHOICE = {
-    "fp32": {1: 1, 2: 1, 3: 4, 4: 5, 5: 5, 6: 1, 7: 0, 8: 4, 9: 0, 10: 1, 11: 6, 12: 5, 13: 0},
-    "fp64": {1: 1, 2: 2, 3: 3, 4: 4, 5: 4, 6: 4, 7: 0, 8: 2, 9: 1, 10: 2, 11: 1, 12: 3, 13: 2},
+    "fp32": {1: 1, 2: 1, 3: 4, 4: 5, 5: 5, 6: 1, 7: 0, 8: 4, 9: 0, 10: 1, 11: 6, 12: 6, 13: 8},
+    "fp64": {1: 1, 2: 2, 3: 3, 4: 4, 5: 4, 6: 4, 7: 0, 8: 2, 9: 1, 10: 2, 11: 4, 12: 4, 13: 2},
 }
 ELEM_BYTES = {"fp32": 8, "fp64": 16}
 CTYPE = {"fp32": "float", "fp64": "double"}
@@ -187,8 +187,10 @@ def single_configs(all_candidates=True):
                 ex = (n + (n >> ps) + 1 if ps else n) if len(radices) > 1 else 0
                 st = n + 1 if c["stage"] in (1, 3) else (n if c["stage"] == 4 else 0)
                 ib = s * n if c["stage"] in (2, 3) else 0  # TMA prefetch buffer
-                smem = ((ib + s * max(ex, st)) * ELEM_BYTES[prec]
-                        + 10 * (threads // 32 + 1) * (ELEM_BYTES[prec] // 2))  # 5 sums per warp, x2 parity
+                # ABFT scratch: per-warp sums (TPS <= 32) or the deferred
+                # two-tile reduction pipeline (TPS >= 128: 2 x S x 5 x TPS partials + totals)
+                red = 10 * (threads // 32 + 1) + (10 * threads + 10 * s if tps >= 128 else 0)
+                smem = (ib + s * max(ex, st)) * ELEM_BYTES[prec] + red * (ELEM_BYTES[prec] // 2)
                 out.append(dict(prec=prec, logn=logn, n=n, e=e, radices=radices, threads=threads,
                                 ps=ps, smem=smem, tps=tps, minb=c["minb"], stage=c["stage"],
                                 variant=vi, chosen=vi == chosen))

@@ -305,10 +305,20 @@ fft_single_kernel(const SingleArgs<T> a) {
             }
         }
     };
-    // TPS > 32: the previous tile's cross-warp sums, published through this
-    // tile's first barrier (double-buffered by tile parity)
+    // TPS > 32: the cross-thread sums run as a two-tile pipeline through the
+    // barriers the next tiles already have (no extra barrier, few shuffles):
+    //   end of tile i     : every thread stores its 5 partials (part[par]);
+    //   tile i+1 (stage 1): the signal's warps reduce them, warp w taking sums
+    //                       w, w + TPS/32, ... (strided LDS + 5 shuffles), and
+    //                       store the totals (tot[par]);
+    //   tile i+2 (stage 2): thread t == 0 decides tile i.
+    // Summation order is fixed (deterministic rel values).
+    // 32 < TPS < 128 (two or three warps per signal): one-tile deferral — the
+    // warps shuffle their sums fully, lanes 0 store them (parity-buffered), and
+    // thread t == 0 adds the few warp totals after the next tile's barrier.
     constexpr bool TB = ABFT == ABFT_WANG || ABFT == ABFT_TABLE;  // threadblock-level checksums
-    constexpr bool DEFER = TB && TPS > 32;
+    constexpr bool DEFER1 = TB && TPS > 32 && TPS < 128;
+    constexpr bool DEFER = TB && TPS >= 128;
     bool pend = false, pend_live = false;
     long long pend_b = 0;
     unsigned pend_par = 0;
@@ -329,6 +339,44 @@ fft_single_kernel(const SingleArgs<T> a) {
         decide_signal(sums, pend_b, owner);
         pend = false;
     };
+    constexpr int NWS = TPS > 32 ? TPS / 32 : 1;  // warps per signal
+    constexpr int PPS = TPS;                         // stored partials per sum per signal
+    T* const part = red;                             // [2][S][5][PPS]
+    T* const tot = red + 2 * S * 5 * PPS;            // [2][S][5]
+    bool p1 = false, p1_live = false, p2 = false, p2_live = false;
+    long long p1_b = 0, p2_b = 0;
+    unsigned p1_par = 0, p2_par = 0;
+    auto stage_reduce = [&]() {  // tile held in p1 -> totals; moves it to p2
+        const int ws = t >> 5, lane = threadIdx.x & 31;
+        const T* pp = part + ((size_t)p1_par * S + sl) * 5 * PPS;
+#pragma unroll
+        for (int i0 = 0; i0 < 5; i0 += NWS) {
+            const int i = i0 + ws;
+            if (i < 5) {  // warp-uniform
+                T acc = lane < PPS ? pp[i * PPS + lane] : T(0);
+#pragma unroll
+                for (int k = 1; k < (PPS + 31) / 32; ++k) acc = fadd(acc, pp[i * PPS + k * 32 + lane]);
+#pragma unroll
+                for (int off = 16; off >= 1; off >>= 1) acc = fadd(acc, shfl_xor(acc, off));
+                if (lane == 0) tot[((size_t)p1_par * S + sl) * 5 + i] = acc;
+            }
+        }
+        p2 = true;
+        p2_live = p1_live;
+        p2_b = p1_b;
+        p2_par = p1_par;
+        p1 = false;
+    };
+    auto stage_decide = [&]() {  // tile held in p2
+        T sums[5] = {T(0), T(0), T(0), T(0), T(0)};
+        const bool owner = t == 0 && p2_live;
+        if (owner) {
+#pragma unroll
+            for (int i = 0; i < 5; ++i) sums[i] = tot[((size_t)p2_par * S + sl) * 5 + i];
+        }
+        decide_signal(sums, p2_b, owner);
+        p2 = false;
+    };
     unsigned iter = 0;
     for (long long tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++iter) {
         const long long b = tile * S + sl;
@@ -339,8 +387,11 @@ fft_single_kernel(const SingleArgs<T> a) {
 
         // input-side ABFT row e^T W at this thread's positions (the same for
         // every tile: L1 hits), requested before the tile data is waited for
+#ifndef TFFT_EW_HOIST
+#define TFFT_EW_HOIST 1
+#endif
         C<T> ew[TB ? E : 1];
-        if constexpr (TB) {
+        if constexpr (TB && TFFT_EW_HOIST) {
 #pragma unroll
             for (int m = 0; m < E; ++m) ew[m] = __ldg(a.etw + t + m * TPS);
         }
@@ -408,6 +459,7 @@ fft_single_kernel(const SingleArgs<T> a) {
         if constexpr (TB) {
 #pragma unroll
             for (int m = 0; m < E; ++m) {
+                if constexpr (!TFFT_EW_HOIST) ew[m] = __ldg(a.etw + t + m * TPS);
                 if constexpr (!(TFFT_ABLATE & 2)) cin = cmac<T>(cin, v[m], ew[m]);
                 if constexpr (!(TFFT_ABLATE & 4)) l1p = cadd<T>(l1p, cabs2<T>(v[m]));
             }
@@ -455,8 +507,12 @@ fft_single_kernel(const SingleArgs<T> a) {
 #pragma unroll
             for (int m = 0; m < E; ++m) v[m] = swapri<T>(v[m]);
         }
-        if constexpr (DEFER) {
-            if (pend) finish_pending();  // the exchanges above contain barriers
+        if constexpr (DEFER) {  // the exchanges above contain barriers
+            if (p2) stage_decide();
+            if (p1) stage_reduce();
+        }
+        if constexpr (DEFER1) {
+            if (pend) finish_pending();
         }
         if (fault_here && fw == AT_PRESCALE) {
 #pragma unroll
@@ -559,6 +615,14 @@ fft_single_kernel(const SingleArgs<T> a) {
             }
             T sums[5] = {cin.x, cin.y, cout.x, cout.y, fadd(l1p.x, l1p.y)};
             if constexpr (DEFER) {
+                T* pp = part + ((size_t)(iter & 1) * S + sl) * 5 * PPS + t;
+#pragma unroll
+                for (int i = 0; i < 5; ++i) pp[i * PPS] = sums[i];
+                p1 = true;
+                p1_live = live;
+                p1_b = b;
+                p1_par = iter & 1;
+            } else if constexpr (DEFER1) {
                 if constexpr (!(TFFT_ABLATE & 1)) warp_partials<5>(sums, red + (size_t)(iter & 1) * NW * 5);
                 pend = true;
                 pend_live = live;
@@ -570,10 +634,21 @@ fft_single_kernel(const SingleArgs<T> a) {
             }
         }
     }
-    if constexpr (DEFER) {
+    if constexpr (DEFER1) {
         if (pend) {
             __syncthreads();
             finish_pending();
+        }
+    }
+    if constexpr (DEFER) {  // drain the pipeline (uniform across the CTA)
+        if (p1 || p2) {
+            __syncthreads();
+            if (p2) stage_decide();
+            if (p1) {
+                stage_reduce();
+                __syncthreads();
+                stage_decide();
+            }
         }
     }
     if constexpr (ABFT != ABFT_OFF) {

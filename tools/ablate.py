@@ -17,6 +17,10 @@ def child(logn):
     from paper_2405_02520_b200.fft_core import fit_group_size
     from paper_2405_02520_b200.fft_core.plan import native_plan
     lib = _lib.load()
+    for spec in filter(None, os.environ.get("TFFT_VARIANTS", "").split(",")):
+        ln, var = (int(v) for v in spec.split(":"))
+        if ln == logn:
+            _lib.check(lib.tfft_tune_select(0, ln, var))
     n = 1 << logn
     b = (1 << 30) // (8 * n)
     x = torch.randn(b * n, dtype=torch.complex64, device="cuda")
@@ -40,18 +44,21 @@ def child(logn):
             if i >= 2:
                 ts.append(e0.elapsed_time(e1))
         out[sc] = round(sorted(ts)[len(ts) // 2], 4)
-    print(json.dumps({"lib": os.environ.get("TFFT_LIB_PATH", "product"), "n": n, **out}), flush=True)
+    print(json.dumps({"lib": os.path.basename(os.environ.get("TFFT_LIB_PATH", "product")),
+                      "variants": os.environ.get("TFFT_VARIANTS", ""), "n": n, **out}), flush=True)
 
 
 if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "child":
         child(int(sys.argv[2]))
     else:
-        libs = [None, None] + sorted(os.path.join(ROOT, "paper_2405_02520_b200", "ablate", f)
+        libs = [None] + sorted(os.path.join(ROOT, "paper_2405_02520_b200", "ablate", f)
                                for f in os.listdir(os.path.join(ROOT, "paper_2405_02520_b200", "ablate")))
-        for lib in libs:
-            env = dict(os.environ)
-            if lib:
-                env["TFFT_LIB_PATH"] = lib
-            for logn in (11, 12):
-                subprocess.run([sys.executable, __file__, "child", str(logn)], env=env)
+        for variants in ("", "13:7,12:6"):
+            for lib in libs:
+                env = dict(os.environ)
+                env["TFFT_VARIANTS"] = variants
+                if lib:
+                    env["TFFT_LIB_PATH"] = lib
+                for logn in (11, 12, 13):
+                    subprocess.run([sys.executable, __file__, "child", str(logn)], env=env)

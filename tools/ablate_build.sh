@@ -1,19 +1,24 @@
 #!/bin/bash
-# Cost attribution of the fused ABFT: rebuild the single-kernel parts holding
-# N=2048 (part 3) and N=4096 (part 0) with -DTFFT_ABLATE=k and link
-# paper_2405_02520_b200/ablate/libtfft_k.so from the product objects.
+# Experiment builds: rebuild the single-kernel parts holding N = 2048 (part 3),
+# 4096 (part 0) and 8192 (part 1) with extra -D flags and link
+# paper_2405_02520_b200/ablate/libtfft_<tag>.so from the product objects.
+#   bash tools/ablate_build.sh TAG "-DTFFT_ABLATE=1" [TAG2 "-D..."] ...
 set -e
 cd "$(dirname "$0")/../paper_2405_02520_b200"
 mkdir -p ablate build/ablate
 NV="/usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC --expt-relaxed-constexpr -I../include -Icsrc"
-for k in "$@"; do
-  for p in 0 3; do
-    $NV -DTFFT_ABLATE=$k -c csrc/gen_single_fp32_$p.cu -o build/ablate/gen_single_fp32_${p}_$k.o &
+args=("$@")
+for ((i = 0; i < ${#args[@]}; i += 2)); do
+  tag=${args[i]}; flags=${args[i+1]}
+  for p in 0 1 3; do
+    $NV $flags -c csrc/gen_single_fp32_$p.cu -o build/ablate/gen_single_fp32_${p}_$tag.o &
   done
 done
 wait
-for k in "$@"; do
-  objs=$(ls build/*.o | grep -v "gen_single_fp32_0.o\|gen_single_fp32_3.o")
-  $NV -shared -o ablate/libtfft_$k.so $objs build/ablate/gen_single_fp32_0_$k.o build/ablate/gen_single_fp32_3_$k.o -lcudart
+for ((i = 0; i < ${#args[@]}; i += 2)); do
+  tag=${args[i]}
+  objs=$(ls build/*.o | grep -v "gen_single_fp32_[013].o")
+  $NV -shared -o ablate/libtfft_$tag.so $objs build/ablate/gen_single_fp32_0_$tag.o \
+      build/ablate/gen_single_fp32_1_$tag.o build/ablate/gen_single_fp32_3_$tag.o -lcudart
 done
 ls -la ablate
