@@ -465,6 +465,86 @@ __global__ void __launch_bounds__(256) abft_finalize_kernel(const FinalArgs<T> a
     if (threadIdx.x == 0 && cta_max) atomicMax(a.max_key, cta_max);
 }
 
+// Same decision with a whole CTA per signal, for few signals with many tiles
+// (2^23..2^25: 2-8 signals x 8k-130k tiles, where a warp per signal
+// serialised on load latency for ~0.1 ms). Four independent accumulator sets
+// per thread keep loads in flight; fixed combination order (deterministic).
+template <class T>
+__global__ void __launch_bounds__(256) abft_finalize_cta_kernel(const FinalArgs<T> a) {
+    __shared__ T sh[8][5];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    T my_max = T(0);
+    for (long long b = blockIdx.x; b < a.batch; b += gridDim.x) {
+        T acc[4][5];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int k = 0; k < 5; ++k) acc[u][k] = T(0);
+        const T* pin = a.part_in + b * a.tiles_in * 3;
+        long long i = threadIdx.x;
+        for (; i + 3 * 256 < a.tiles_in; i += 4 * 256) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const T* p = pin + (i + u * 256) * 3;
+                acc[u][0] = fadd(acc[u][0], p[0]); acc[u][1] = fadd(acc[u][1], p[1]); acc[u][2] = fadd(acc[u][2], p[2]);
+            }
+        }
+        for (; i < a.tiles_in; i += 256) {
+            const T* p = pin + i * 3;
+            acc[0][0] = fadd(acc[0][0], p[0]); acc[0][1] = fadd(acc[0][1], p[1]); acc[0][2] = fadd(acc[0][2], p[2]);
+        }
+        const T* pout = a.part_out + b * a.tiles_out * 2;
+        i = threadIdx.x;
+        for (; i + 3 * 256 < a.tiles_out; i += 4 * 256) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const T* p = pout + (i + u * 256) * 2;
+                acc[u][3] = fadd(acc[u][3], p[0]); acc[u][4] = fadd(acc[u][4], p[1]);
+            }
+        }
+        for (; i < a.tiles_out; i += 256) {
+            const T* p = pout + i * 2;
+            acc[0][3] = fadd(acc[0][3], p[0]); acc[0][4] = fadd(acc[0][4], p[1]);
+        }
+        T v[5];
+#pragma unroll
+        for (int k = 0; k < 5; ++k) {
+            v[k] = fadd(fadd(acc[0][k], acc[1][k]), fadd(acc[2][k], acc[3][k]));
+#pragma unroll
+            for (int off = 16; off >= 1; off >>= 1) v[k] = fadd(v[k], shfl_xor(v[k], off));
+        }
+        if (lane == 0) {
+#pragma unroll
+            for (int k = 0; k < 5; ++k) sh[warp][k] = v[k];
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            T t5[5];
+#pragma unroll
+            for (int k = 0; k < 5; ++k) {
+                t5[k] = sh[0][k];
+                for (int w = 1; w < 8; ++w) t5[k] = fadd(t5[k], sh[w][k]);
+            }
+            T rel, rel2;
+            bool flagged, recheck;
+            abft_decide<T>(t5[0], t5[1], t5[3], t5[4], t5[2], a.delta, a.abs_floor, a.floor_coef, true, rel, rel2,
+                           flagged, recheck);
+            if (recheck) rel = T(-1);
+            else my_max = my_max > rel ? my_max : rel;
+            if (a.rel_out) a.rel_out[b] = rel;
+            if (flagged || recheck) {
+                const int slot = atomicAdd(a.flag_count, 1);
+                if (slot < a.flag_cap) {
+                    a.flag_sig[slot] = a.sig_base + b;
+                    a.flag_rel[slot] = rel;
+                }
+            }
+        }
+        __syncthreads();  // sh reused by the next signal
+    }
+    if (threadIdx.x == 0 && my_max > T(0)) atomicMax(a.max_key, order_key(my_max));
+}
+
 // ------------------------------------------------------------------ host
 struct PassEntry {
     int logl;

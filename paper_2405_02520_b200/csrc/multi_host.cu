@@ -402,8 +402,13 @@ int multi_launch_t(MultiPlan& mp, const MultiLaunch& m, cudaStream_t st) {
         f.flag_cap = m.flag_cap;
         f.max_key = (typename KeyT<T>::type*)m.max_key;
         f.rel_out = (T*)m.rel_out;
-        const long long grid = std::min<long long>((m.batch + 7) / 8, 4LL * mp.num_sms);
-        abft_finalize_kernel<T><<<(unsigned)std::max<long long>(grid, 1), 256, 0, st>>>(f);
+        if (tiles[0] >= 1024) {  // few signals, many tiles: a CTA per signal
+            const long long grid = std::min<long long>(m.batch, 4LL * mp.num_sms);
+            abft_finalize_cta_kernel<T><<<(unsigned)std::max<long long>(grid, 1), 256, 0, st>>>(f);
+        } else {                 // a warp per signal
+            const long long grid = std::min<long long>((m.batch + 7) / 8, 4LL * mp.num_sms);
+            abft_finalize_kernel<T><<<(unsigned)std::max<long long>(grid, 1), 256, 0, st>>>(f);
+        }
         MCU(cudaGetLastError());
     }
     return TFFT_OK;
