@@ -154,6 +154,11 @@ int tfft_run_campaign(tfft_plan *plan, const void *in, void *out, int64_t runs,
                       int inverse, double *run_max_rel, int32_t *run_fired,
                       tfft_report *report, void *stream);
 
+/* HBM passes one unfaulted transform of this plan launches (1 for n <= 2^13;
+ * large 2-stage plans execute as 3 short-L passes). The
+ * reference's pass accounting (RunReport.pass_count) is unaffected. */
+int tfft_plan_exec_passes(const tfft_plan *plan);
+
 /* Checksum granularity of the protected calls on this plan, for the paper's
  * scheme comparison (TurboFFT one-sided vs thread-level vs threadblock-level;
  * not a reference interface): 0 = threadblock-level two-sided checksums per

@@ -184,6 +184,12 @@ struct tfft_plan {
     void* tw = nullptr;             // w_N^k, k < N (single-kernel path)
     // multi-pass path
     MultiPlan multi;
+    // Execution-only 3-pass split for large 2-stage plans (short L per pass;
+    // the API plan's L = 1024..2048 passes read 32-64 B row segments). Used
+    // whenever no stage:k hook coordinates are involved; the API plan keeps
+    // execute_stage and stage faults. pass_count is the API plan's.
+    MultiPlan fast;
+    bool have_fast = false;
     // workspace
     Counters* d_cnt = nullptr;
     Counters* h_cnt = nullptr;      // pinned
@@ -323,7 +329,10 @@ int launch_transform(tfft_plan* p, const Launch& L, cudaStream_t st) {
     m.nfaults = L.nfaults;
     m.f_div = L.f_div;
     m.rel_out = L.rel_out;
-    int rc = multi_launch(p->multi, m, st);
+    bool api_layout = L.f_where == 2;  // a stage:k fault addresses the API plan's intermediates
+    for (long long r = 0; L.faults && r < L.nfaults && !api_layout; ++r) api_layout = L.faults[r].where == 2;
+    MultiPlan& mp = (p->have_fast && !api_layout) ? p->fast : p->multi;
+    int rc = multi_launch(mp, m, st);
     if (rc) return fail(rc, multi_last_error());
     return TFFT_OK;
 }
@@ -570,6 +579,19 @@ int tfft_plan_create(tfft_plan** out, int64_t n, int precision, int nstages, con
     } else {
         rc = multi_plan_init(p->multi, n, precision, nstages, dims, p->num_sms);
         if (rc) return cleanup(fail(rc, multi_last_error()));
+        // measured crossover (profiles/sweep_r01_*): fp32 from 2^21, fp64 from 2^19
+        static const int fast_env = [] {
+            const char* e = getenv("TFFT_FAST3_MIN_LOGN");  // tuning override
+            return e ? atoi(e) : 0;
+        }();
+        const int fast_min = fast_env ? fast_env : (precision == TFFT_FP32 ? 21 : 19);
+        if (nstages == 2 && p->logn >= fast_min) {
+            const int q = p->logn / 3, r = p->logn % 3;  // balanced, larger parts last
+            int64_t d3[3];
+            for (int i = 0; i < 3; ++i) d3[i] = int64_t(1) << (q + (i >= 3 - r ? 1 : 0));
+            p->have_fast = multi_plan_init(p->fast, n, precision, 3, d3, p->num_sms) == TFFT_OK;
+            if (!p->have_fast) multi_plan_free(p->fast);
+        }
     }
     if (cudaMalloc(&p->d_cnt, sizeof(Counters)) != cudaSuccess) return cleanup(fail(TFFT_ENOMEM, "counters"));
     if (cudaMallocHost(&p->h_cnt, sizeof(Counters)) != cudaSuccess) return cleanup(fail(TFFT_ENOMEM, "pinned counters"));
@@ -582,6 +604,7 @@ int tfft_plan_destroy(tfft_plan* p) {
     cudaSetDevice(p->device);
     cudaFree(p->tw);
     multi_plan_free(p->multi);
+    if (p->have_fast) multi_plan_free(p->fast);
     cudaFree(p->d_cnt);
     cudaFreeHost(p->h_cnt);
     cudaFree(p->d_flag_sig);
@@ -1585,6 +1608,16 @@ int tfft_set_check_level(tfft_plan* p, int level) {
     if (level == 1 && !p->single) return fail(TFFT_EUNSUPPORTED, "thread-level checks are built for n <= 2^13");
     p->check_level = level;
     return TFFT_OK;
+}
+
+}  // extern "C"
+
+extern "C" {
+
+int tfft_plan_exec_passes(const tfft_plan* p) {
+    if (!p) return -1;
+    if (p->single) return 1;
+    return p->have_fast ? 3 : p->nstages;
 }
 
 }  // extern "C"

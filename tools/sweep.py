@@ -87,9 +87,9 @@ def main():
 
             t_on, t_off = timed(on), timed(off)
             t_cu = None if args.no_cufft else timed(cufft)
-            passes = 1 if n <= 8192 else len(plan.stages)
+            passes = lib.tfft_plan_exec_passes(h.handle)  # HBM passes actually launched
             byts = 2.0 * b * n * es
-            r = dict(prec=prec, n=n, batch=b, passes=passes, ms_on=round(t_on, 4),
+            r = dict(prec=prec, n=n, batch=b, passes=passes, api_stages=len(plan.stages), ms_on=round(t_on, 4),
                      ms_off=round(t_off, 4), ms_cufft=None if t_cu is None else round(t_cu, 4),
                      gbs_pass_on=round(passes * byts / t_on / 1e6, 1),
                      frac_pass_on=round(passes * byts / t_on / 1e6 / peak, 4),
