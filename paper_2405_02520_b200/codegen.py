@@ -257,10 +257,12 @@ def _pc(*rows):
 PASS_CANDIDATES = {
     "fp32": {
         1: _pc((2, (2,), 16, 1, 0)), 2: _pc((4, (4,), 16, 1, 0)), 3: _pc((8, (8,), 16, 1, 0)),
-        4: _pc((16, (16,), 16, 1, 0)), 5: _pc((8, (8, 4), 16, 1, 0)), 6: _pc((8, (8, 8), 16, 1, 0)),
+        4: _pc((16, (16,), 16, 1, 0)), 5: _pc((8, (8, 4), 16, 1, 0)),
+        6: _pc((8, (8, 8), 16, 1, 0), (8, (8, 8), 32, 2, 3), (8, (8, 8), 16, 3, 3), (8, (8, 8), 32, 2, 2),
+               (8, (8, 8), 16, 3, 2)),
         7: _pc((16, (16, 8), 16, 1, 0), (16, (16, 8), 16, 2, 1), (16, (16, 8), 8, 3, 1),
                (8, (8, 8, 2), 16, 2, 1), (16, (16, 8), 16, 2, 2), (16, (16, 8), 8, 3, 2),
-               (16, (16, 8), 16, 2, 3), (16, (16, 8), 8, 3, 3)),
+               (16, (16, 8), 16, 2, 3), (16, (16, 8), 8, 3, 3), (16, (16, 8), 32, 1, 3)),
         8: _pc((16, (16, 16), 16, 1, 0), (16, (16, 16), 16, 2, 1), (16, (16, 16), 8, 3, 1),
                (16, (16, 16), 8, 2, 0), (16, (16, 16), 16, 2, 2), (16, (16, 16), 8, 3, 2),
                (16, (16, 16), 16, 2, 3), (16, (16, 16), 8, 3, 3)),
@@ -276,10 +278,12 @@ PASS_CANDIDATES = {
     },
     "fp64": {
         1: _pc((2, (2,), 8, 1, 0)), 2: _pc((4, (4,), 8, 1, 0)), 3: _pc((8, (8,), 8, 1, 0)),
-        4: _pc((16, (16,), 8, 1, 0)), 5: _pc((8, (8, 4), 8, 1, 0)), 6: _pc((8, (8, 8), 8, 1, 0)),
+        4: _pc((16, (16,), 8, 1, 0)), 5: _pc((8, (8, 4), 8, 1, 0)),
+        6: _pc((8, (8, 8), 8, 1, 0), (8, (8, 8), 16, 2, 3), (8, (8, 8), 8, 3, 3), (8, (8, 8), 16, 2, 2),
+               (8, (8, 8), 8, 3, 2)),
         7: _pc((16, (16, 8), 8, 1, 0), (16, (16, 8), 8, 2, 1), (16, (16, 8), 4, 3, 1),
                (8, (8, 8, 2), 8, 2, 1), (16, (16, 8), 8, 2, 2), (16, (16, 8), 4, 3, 2),
-               (16, (16, 8), 8, 2, 3), (16, (16, 8), 4, 3, 3)),
+               (16, (16, 8), 8, 2, 3), (16, (16, 8), 4, 3, 3), (16, (16, 8), 16, 1, 3)),
         8: _pc((16, (16, 16), 8, 1, 0), (16, (16, 16), 8, 2, 1), (16, (16, 16), 4, 2, 1),
                (8, (8, 8, 4), 8, 2, 1), (16, (16, 16), 8, 2, 2), (8, (8, 8, 4), 8, 2, 2),
                (16, (16, 16), 8, 2, 3), (8, (8, 8, 4), 8, 2, 3)),
@@ -297,8 +301,8 @@ PASS_CANDIDATES = {
 # (first, middle, last) variant per log2 L; missing -> (0, 0, 0).
 # Source: tools/tune_pass.py on a B200, ABFT on, 1 GiB (profiles/tune_pass_r01.json).
 PASS_CHOICE = {
-    "fp32": {7: (6, 6, 5), 8: (6, 6, 5), 9: (6, 0, 7), 10: (7, 0, 8), 11: (6, 0, 6)},
-    "fp64": {7: (3, 6, 4), 8: (7, 6, 4), 9: (7, 0, 5), 10: (6, 0, 6), 11: (0, 0, 3)},
+    "fp32": {7: (6, 6, 5), 8: (6, 6, 5), 9: (6, 0, 7), 10: (7, 0, 6), 11: (6, 0, 6)},
+    "fp64": {6: (1, 1, 0), 7: (8, 8, 8), 8: (6, 6, 4), 9: (2, 0, 7), 10: (6, 0, 6), 11: (0, 0, 3)},
 }
 
 

@@ -59,7 +59,13 @@ def main():
             nst = len(plan.stages)
             small = torch.randn(2, n, dtype=dt, device="cuda")
             ref = np.fft.fft(small.cpu().numpy().astype(np.complex128), axis=-1)
-            for k, d in enumerate(plan.dims):
+            dims = list(plan.dims)
+            if lib.tfft_plan_exec_passes(h.handle) == 3 and nst == 2:
+                # executed as the library's balanced 3-pass split (larger parts last)
+                q, r3 = divmod(logn, 3)
+                dims = [1 << (q + (1 if i >= 3 - r3 else 0)) for i in range(3)]
+                nst = 3
+            for k, d in enumerate(dims):
                 logl = d.bit_length() - 1
                 kind = 0 if k == 0 else (2 if k == nst - 1 else 1)
                 if (logl, kind) in best:
