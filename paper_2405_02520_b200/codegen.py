@@ -38,9 +38,12 @@ SINGLE_CANDIDATES = {
                   (4, (4, 4), 256, 1, 1), (16, (16,), 128, 1, 1), (16, (16,), 128, 1, 3),
                   (8, (8, 2), 256, 1, 3)),
         5: _cands((8, (8, 4), 256, 1, 1), (8, (8, 4), 256, 1, 0), (16, (16, 2), 256, 1, 1),
-                  (32, (32,), 256, 1, 1), (8, (8, 4), 256, 1, 3), (8, (8, 4), 256, 1, 2)),
+                  (32, (32,), 256, 1, 1), (8, (8, 4), 256, 1, 3), (8, (8, 4), 256, 1, 2),
+                  (8, (8, 4), 256, 1, 5), (8, (8, 4), 256, 2, 5), (16, (16, 2), 256, 1, 5),
+                  (4, (4, 4, 2), 256, 2, 5)),
         6: _cands((8, (8, 8), 256, 1, 1), (8, (8, 8), 256, 1, 0), (16, (16, 4), 256, 1, 1),
-                  (16, (16, 4), 256, 1, 0), (8, (8, 8), 256, 1, 3), (8, (8, 8), 256, 1, 2)),
+                  (16, (16, 4), 256, 1, 0), (8, (8, 8), 256, 1, 3), (8, (8, 8), 256, 1, 2),
+                  (8, (8, 8), 256, 1, 5), (8, (8, 8), 256, 2, 5)),
         7: _cands((16, (16, 8), 256, 1, 0), (16, (16, 8), 256, 1, 1), (8, (8, 8, 2), 256, 1, 0),
                   (16, (16, 8), 256, 3, 0), (16, (16, 8), 256, 1, 2)),
         8: _cands((16, (16, 16), 256, 1, 0), (16, (16, 16), 256, 3, 0), (8, (8, 8, 4), 256, 1, 0),
@@ -74,7 +77,7 @@ SINGLE_CANDIDATES = {
         4: _cands((16, (16,), 256, 1, 1), (8, (8, 2), 256, 1, 1), (4, (4, 4), 256, 1, 1),
                   (8, (8, 2), 256, 1, 3), (16, (16,), 128, 1, 3)),
         5: _cands((8, (8, 4), 256, 1, 1), (8, (8, 4), 256, 1, 0), (16, (16, 2), 256, 1, 1),
-                  (8, (8, 4), 256, 1, 3), (8, (8, 4), 256, 1, 2)),
+                  (8, (8, 4), 256, 1, 3), (8, (8, 4), 256, 1, 2), (8, (8, 4), 256, 1, 5)),
         6: _cands((8, (8, 8), 256, 1, 1), (8, (8, 8), 256, 1, 0), (16, (16, 4), 256, 1, 0),
                   (8, (8, 8), 256, 1, 3), (8, (8, 8), 256, 1, 2)),
         7: _cands((16, (16, 8), 256, 1, 0), (8, (8, 8, 2), 256, 1, 0), (16, (16, 8), 256, 1, 1),
@@ -98,8 +101,8 @@ SINGLE_CANDIDATES = {
 # tuned winners (index into SINGLE_CANDIDATES[prec][logn]); missing -> 0.
 # Source: tools/tune.py on a B200, ABFT on, 1 GiB batches (profiles/tune_r01.json).
 SINGLE_CHOICE = {
-    "fp32": {1: 1, 2: 1, 3: 4, 4: 5, 5: 5, 6: 1, 7: 0, 8: 4, 9: 0, 10: 1, 11: 6, 12: 6, 13: 8},
-    "fp64": {1: 1, 2: 2, 3: 3, 4: 4, 5: 4, 6: 4, 7: 0, 8: 2, 9: 1, 10: 2, 11: 4, 12: 4, 13: 2},
+    "fp32": {1: 1, 2: 1, 3: 4, 4: 5, 5: 6, 6: 7, 7: 0, 8: 4, 9: 0, 10: 1, 11: 6, 12: 6, 13: 8},
+    "fp64": {1: 1, 2: 2, 3: 3, 4: 4, 5: 5, 6: 4, 7: 0, 8: 2, 9: 1, 10: 2, 11: 4, 12: 4, 13: 2},
 }
 ELEM_BYTES = {"fp32": 8, "fp64": 16}
 CTYPE = {"fp32": "float", "fp64": "double"}
@@ -187,6 +190,8 @@ def single_configs(all_candidates=True):
                 ex = (n + (n >> ps) + 1 if ps else n) if len(radices) > 1 else 0
                 st = n + 1 if c["stage"] in (1, 3) else (n if c["stage"] == 4 else 0)
                 ib = s * n if c["stage"] in (2, 3) else 0  # TMA prefetch buffer
+                if c["stage"] == 5:  # per-signal rows into padded slots
+                    ib = s * (n + 32 // ELEM_BYTES[prec])
                 # ABFT scratch: per-warp sums (TPS <= 32) or the deferred
                 # two-tile reduction pipeline (TPS >= 128: 2 x S x 5 x TPS partials + totals)
                 red = 10 * (threads // 32 + 1) + (10 * threads + 10 * s if tps >= 128 else 0)
@@ -217,7 +222,7 @@ def _emit_single(prec, cfgs, part, table=False):
                        f"{abft}, {c['threads']}, {c['minb']}, {c['stage']}, RList<{rl}>>")
         entries.append(
             f"    {{{c['logn']}, {c['variant']}, {int(c['chosen'])}, {c['e']}, {c['threads']}, "
-            f"{c['smem']}, {c['tps']}, {{{', '.join(fns)}}}}},  // radices {rl}, pad 2^{c['ps']}, "
+            f"{c['smem']}, {c['tps']}, {c['stage']}, {{{', '.join(fns)}}}}},  // radices {rl}, pad 2^{c['ps']}, "
             f"minb {c['minb']}, stage {c['stage']}")
     lines.append(f"extern const SingleEntry kSingle_{prec}_{part}[] = {{")
     lines += entries

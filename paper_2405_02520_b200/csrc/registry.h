@@ -11,6 +11,7 @@ struct SingleEntry {
     int threads;     // CTA size
     int smem;        // dynamic shared memory bytes
     int tps;         // threads per signal
+    int stage;       // load strategy (STAGE template argument; 5 needs a tensor map)
     const void* fn[4];  // ABFT off / Wang / table / thread-level (last two only on the chosen variant)
 };
 

@@ -13,6 +13,8 @@
 // The cross-batch (right-side) combination s0 = sum_b x_b is rebuilt from the
 // preserved input only for flagged groups ("s0").
 #pragma once
+#include <cuda.h>  // CUtensorMap (STAGE 5 tile loads)
+
 #include "engine.cuh"
 
 namespace tfft {
@@ -43,8 +45,18 @@ struct FaultRec {
     int idx, signal, where, comp, bit, pad;
 };
 
+// 2-D tensor TMA (SASS UTMALDG) of one box into shared memory
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                            unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+        ::"r"(smem_u32(dst)), "l"(reinterpret_cast<unsigned long long>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
+}
+
 template <class T>
-struct SingleArgs {
+struct alignas(64) SingleArgs {
+    CUtensorMap tmap;       // STAGE 5: (batch x N) rows, box S x (N + pad) (OOB pad columns zero-filled)
     const C<T>* in;
     C<T>* out;
     long long batch;        // signals in this launch
@@ -226,7 +238,7 @@ __device__ __forceinline__ void stage_out(C<T>* __restrict__ dst, long long vali
 
 template <class T, int N, int E, int PS, int ABFT, int THREADS, int MINB, int STAGE, class Radices>
 __global__ void __launch_bounds__(THREADS, MINB)
-fft_single_kernel(const SingleArgs<T> a) {
+fft_single_kernel(const __grid_constant__ SingleArgs<T> a) {
     using Eng = Engine<T, N, E, Radices>;
     constexpr int TPS = N / E;
     constexpr int S = THREADS / TPS;  // signals per CTA
@@ -241,9 +253,17 @@ fft_single_kernel(const SingleArgs<T> a) {
     // itself (linear layout) once the last exchange of the current tile has
     // been read, so prefetching costs no extra shared memory (two CTAs/SM at
     // N = 8192).
+    // 5: one 2-D tensor TMA per tile whose box is 4 (complex64) / 2
+    // (complex128) elements WIDER than a signal: the out-of-bounds columns are
+    // zero-filled, so signals land at a padded stride and the t + m*TPS reads
+    // of one warp's signals fall on different banks (a linear chunk puts them
+    // all on the same banks: 8-way conflicts at N = 32).
     constexpr bool STG = STAGE == 1 || STAGE == 3;
-    constexpr bool PF = STAGE == 2 || STAGE == 3;
+    constexpr bool PF = STAGE == 2 || STAGE == 3 || STAGE == 5;
     constexpr bool PFI = STAGE == 4;
+    constexpr bool PFR = STAGE == 5;
+    constexpr int SLP = PFR ? N + 32 / (int)sizeof(C<T>) : N;  // prefetch slot stride (elements)
+    static_assert(!PFR || (SLP * (int)sizeof(C<T>) / 4 <= 256 && S <= 256), "tensor-TMA box limits");
     static_assert(!PFI || TPS > 32, "in-place prefetch needs CTA-wide exchange barriers");
     constexpr bool MULTIPASS = RCount<Radices>::v > 1;
     constexpr int SL = SliceLen<N, PS, MULTIPASS, STG, PFI>::v;
@@ -251,7 +271,7 @@ fft_single_kernel(const SingleArgs<T> a) {
 
     extern __shared__ __align__(128) unsigned char smem_raw[];
     C<T>* ib = reinterpret_cast<C<T>*>(smem_raw);  // prefetch buffer (PF)
-    C<T>* sm_all = ib + (PF ? S * N : 0);
+    C<T>* sm_all = ib + (PF ? S * SLP : 0);
     T* red = reinterpret_cast<T*>(sm_all + S * SL);  // 5 partial sums per warp
     __shared__ typename KeyT<T>::type cta_max;
     __shared__ unsigned long long in_bar;
@@ -264,16 +284,23 @@ fft_single_kernel(const SingleArgs<T> a) {
 
     const long long tiles = (a.batch + S - 1) / S;
     C<T>* const pf_dst = PFI ? sm_all : ib;
-    auto prefetch = [&](long long tl) {  // thread 0 only
+    auto prefetch = [&](long long tl) {  // thread 0 only (PFR: threads 0..S-1, one row each)
         const long long nsig = (a.batch - tl * S) < S ? (a.batch - tl * S) : S;
-        const unsigned bytes = (unsigned)(nsig * N * sizeof(C<T>));
-        mbar_expect_tx(&in_bar, bytes);
-        bulk_g2s(pf_dst, a.in + tl * S * N, bytes, &in_bar);
+        if constexpr (PFR) {  // the full box arrives, OOB rows / columns as zeros
+            (void)nsig;
+            mbar_expect_tx(&in_bar, (unsigned)(S * SLP * sizeof(C<T>)));
+            tma_load_2d(pf_dst, &a.tmap, 0, (int)(tl * S), &in_bar);
+        } else {
+            const unsigned bytes = (unsigned)(nsig * N * sizeof(C<T>));
+            mbar_expect_tx(&in_bar, bytes);
+            bulk_g2s(pf_dst, a.in + tl * S * N, bytes, &in_bar);
+        }
     };
+    constexpr int ISSUE = 1;  // the thread that issues (and arrives on) each prefetch
     if constexpr (PF || PFI) {
-        if (threadIdx.x == 0) mbar_init(&in_bar, 1);
+        if (threadIdx.x == 0) mbar_init(&in_bar, ISSUE);
         __syncthreads();
-        if (threadIdx.x == 0 && blockIdx.x < tiles) prefetch(blockIdx.x);
+        if (threadIdx.x < ISSUE && blockIdx.x < tiles) prefetch(blockIdx.x);
     }
     // Detection decision of one signal from its five reduced sums and the
     // warp-aggregated append of flagged / recheck signals (rare). Every lane
@@ -430,9 +457,9 @@ fft_single_kernel(const SingleArgs<T> a) {
         } else if constexpr (PF) {
             mbar_wait(&in_bar, iter & 1);
 #pragma unroll
-            for (int m = 0; m < E; ++m) v[m] = live ? ib[sl * N + t + m * TPS] : mk<T>(T(0), T(0));
+            for (int m = 0; m < E; ++m) v[m] = live ? ib[sl * SLP + t + m * TPS] : mk<T>(T(0), T(0));
             __syncthreads();  // everyone has the tile in registers: refill the buffer
-            if (threadIdx.x == 0 && tile + gridDim.x < tiles) {
+            if (threadIdx.x < ISSUE && tile + gridDim.x < tiles) {
                 fence_proxy_async();
                 prefetch(tile + gridDim.x);
             }

@@ -262,6 +262,33 @@ struct Launch {
     void* rel_out;
 };
 
+// STAGE 5 tensor map: (batch x N) complex rows as 32-bit words; box of S rows
+// x (N + pad) elements, pad = 32 B, so each row lands at a padded smem stride.
+int encode_single_tmap(CUtensorMap* map, const void* base, int64_t n, int64_t batch, int esize, int S) {
+    using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    static EncodeFn fn = [] {
+        void* q = nullptr;
+        cudaDriverEntryPointQueryResult r;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &q, cudaEnableDefault, &r) != cudaSuccess ||
+            r != cudaDriverEntryPointSuccess)
+            return (EncodeFn) nullptr;
+        return (EncodeFn)q;
+    }();
+    if (!fn) return fail(TFFT_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    const cuuint64_t cw = esize / 4;
+    cuuint64_t dims[2] = {cw * (cuuint64_t)n, (cuuint64_t)batch};
+    cuuint64_t strides[1] = {(cuuint64_t)n * esize};
+    cuuint32_t box[2] = {(cuuint32_t)(cw * (n + 32 / esize)), (cuuint32_t)S};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<void*>(base), dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(TFFT_ECUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+    return TFFT_OK;
+}
+
 template <class T>
 int launch_single_t(tfft_plan* p, const Launch& L, cudaStream_t st) {
     const SingleEntry* e = single_entry(p->prec, p->logn, L.abft);
@@ -299,6 +326,10 @@ int launch_single_t(tfft_plan* p, const Launch& L, cudaStream_t st) {
     a.f_bit = L.f_bit;
     const int S = e->threads / e->tps;
     const long long tiles = (L.batch + S - 1) / S;
+    if (e->stage == 5) {  // rows as a 2-D tensor, box padded past the signal end
+        int rc2 = encode_single_tmap(&a.tmap, L.in, p->n, L.batch, (int)p->esize, S);
+        if (rc2) return rc2;
+    }
     long long grid = std::min<long long>(tiles, (long long)nb * p->num_sms);
     if (grid < 1) grid = 1;
     void* args[] = {&a};
