@@ -645,7 +645,7 @@ fft_single_kernel(const __grid_constant__ SingleArgs<T> a) {
                 T* pp = part + ((size_t)(iter & 1) * S + sl) * 5 * PPS + t;
 #pragma unroll
                 for (int i = 0; i < 5; ++i) pp[i * PPS] = sums[i];
-                p1 = true;
+                p1 = !(TFFT_ABLATE & 1);
                 p1_live = live;
                 p1_b = b;
                 p1_par = iter & 1;

@@ -54,7 +54,7 @@ if __name__ == "__main__":
     else:
         libs = [None] + sorted(os.path.join(ROOT, "paper_2405_02520_b200", "ablate", f)
                                for f in os.listdir(os.path.join(ROOT, "paper_2405_02520_b200", "ablate")))
-        for variants in ("", "13:7,12:6"):
+        for variants in ("",):
             for lib in libs:
                 env = dict(os.environ)
                 env["TFFT_VARIANTS"] = variants
