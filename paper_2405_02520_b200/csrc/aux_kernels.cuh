@@ -164,6 +164,95 @@ __global__ void group_sums_jobs_kernel(const C<T>* __restrict__ in, long long bs
     }
 }
 
+// The same correction split over many CTAs per group (grid.x chunks of the
+// n points, grid.y groups) for long signals: phase 1 rebuilds its chunk into
+// `scratch` and writes the chunk's (c_in, c_out, l1) partials; phase 2 (one
+// CTA per group) sums them in chunk order and decides; phase 3 commits the
+// verified groups chunk by chunk.
+constexpr int FIX_CHUNK = 2048;  // points per CTA in phase 1 / 3
+template <class T>
+__global__ void __launch_bounds__(256)
+fix_rebuild_kernel(const C<T>* __restrict__ in, const C<T>* __restrict__ out, long long n, long long bs,
+                   const C<T>* __restrict__ ws0, C<T>* __restrict__ scratch, const C<T>* __restrict__ etw,
+                   const C<T>* __restrict__ values, const FixJob* __restrict__ jobs, T* __restrict__ part) {
+    __shared__ T sh[8][5];
+    const FixJob job = jobs[blockIdx.y];
+    const C<T>* w = ws0 + (long long)blockIdx.y * n;
+    C<T>* fx = scratch + (long long)blockIdx.y * n;
+    const C<T>* xf = in + job.flagged * n;
+    const long long k0 = (long long)blockIdx.x * FIX_CHUNK;
+    const long long k1 = k0 + FIX_CHUNK < n ? k0 + FIX_CHUNK : n;
+    C<T> cin = mk<T>(T(0), T(0)), cout = mk<T>(T(0), T(0));
+    T l1 = T(0);
+    const T hr = T(-0.5), hi = T(0.8660254037844386467637232);
+    for (long long k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
+        C<T> others = mk<T>(T(0), T(0));
+        bool first = true;
+        for (long long b = 0; b < bs; ++b) {
+            const long long sg = job.first + b;
+            if (sg == job.flagged) continue;
+            const C<T> v = out[sg * n + k];
+            others = first ? v : cadd<T>(others, v);
+            first = false;
+        }
+        const C<T> f = csub<T>(w[k], others);
+        fx[k] = f;
+        C<T> e;
+        if (values) e = values[k];
+        else {
+            const int cls = (int)(k % 3);
+            e = cls == 0 ? mk<T>(T(1), T(0)) : (cls == 1 ? mk<T>(hr, -hi) : mk<T>(hr, hi));
+        }
+        cout = cadd<T>(cout, cmul<T>(f, e));
+        const C<T> x = xf[k];
+        cin = cadd<T>(cin, cmul<T>(x, etw[k]));
+        l1 = fadd(l1, cabs<T>(x));
+    }
+    T v[5] = {cin.x, cin.y, cout.x, cout.y, l1};
+#pragma unroll
+    for (int i = 0; i < 5; ++i)
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) v[i] = fadd(v[i], shfl_xor(v[i], off));
+    if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+        for (int i = 0; i < 5; ++i) sh[threadIdx.x >> 5][i] = v[i];
+    }
+    __syncthreads();
+    if (threadIdx.x < 5) {
+        T acc = sh[0][threadIdx.x];
+        for (int wv = 1; wv < 8; ++wv) acc = fadd(acc, sh[wv][threadIdx.x]);
+        part[((long long)blockIdx.y * gridDim.x + blockIdx.x) * 5 + threadIdx.x] = acc;
+    }
+}
+
+template <class T>
+__global__ void fix_decide_kernel(long long chunks, const T* __restrict__ part, T delta, T abs_floor,
+                                  T floor_coef, FixJob* jobs) {
+    if (threadIdx.x != 0) return;
+    T a[5] = {T(0), T(0), T(0), T(0), T(0)};
+    for (long long c = 0; c < chunks; ++c)
+#pragma unroll
+        for (int i = 0; i < 5; ++i) a[i] = fadd(a[i], part[((long long)blockIdx.x * chunks + c) * 5 + i]);
+    const C<T> raw = mk<T>(fsub(a[0], a[2]), fsub(a[1], a[3]));
+    const T fl = nanmax<T>(abs_floor, fmul(floor_coef, a[4]));
+    const T den = nanmax<T>(cabs<T>(mk<T>(a[0], a[1])), fl);
+    T r = cabs<T>(raw) / den;
+    if (!isfinite(r)) r = T(INFINITY);
+    jobs[blockIdx.x].ok = !(r > delta);
+}
+
+template <class T>
+__global__ void fix_commit_kernel(C<T>* __restrict__ out, long long n, const C<T>* __restrict__ scratch,
+                                  const FixJob* __restrict__ jobs) {
+    const FixJob job = jobs[blockIdx.y];
+    if (!job.ok) return;
+    const long long k0 = (long long)blockIdx.x * FIX_CHUNK;
+    const long long k1 = k0 + FIX_CHUNK < n ? k0 + FIX_CHUNK : n;
+    const C<T>* fx = scratch + (long long)blockIdx.y * n;
+    C<T>* dst = out + job.flagged * n;
+    for (long long k = k0 + threadIdx.x; k < k1; k += blockDim.x) dst[k] = fx[k];
+}
+
 // Online correction of K flagged groups, one CTA per group:
 //   fixed = W s0 - sum_{b != f} y_b  (pipeline.py:180-185),
 //   then re-verify the rebuilt signal against its input-side checksum and

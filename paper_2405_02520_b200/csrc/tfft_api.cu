@@ -193,6 +193,12 @@ struct tfft_plan {
     // workspace
     Counters* d_cnt = nullptr;
     Counters* h_cnt = nullptr;      // pinned
+    // the first kEarly flag entries ride back with the counters (pinned), so a
+    // rare fault costs no extra host round trip before the decision
+    static constexpr int kEarly = 64;
+    long long* h_flag_sig = nullptr;
+    double* h_flag_rel = nullptr;   // kEarly entries of the plan dtype
+    int64_t early_n = 0;
     long long* d_flag_sig = nullptr;
     void* d_flag_rel = nullptr;
     int64_t flag_cap = 0;
@@ -485,6 +491,21 @@ int64_t groups_per_chunk(const tfft_plan* p, int64_t batch) {
     return std::min<int64_t>(gpc, batch / p->bs);
 }
 
+// The detection summary behind the kernels: counters plus the first kEarly
+// flag entries (only read on the host when flag_count says so), then ev_done.
+int enqueue_summary(tfft_plan* p, cudaStream_t st) {
+    CU(cudaMemcpyAsync(p->h_cnt, p->d_cnt, sizeof(Counters), cudaMemcpyDeviceToHost, st));
+    p->early_n = std::min<int64_t>(tfft_plan::kEarly, p->flag_cap);
+    if (p->early_n > 0) {
+        CU(cudaMemcpyAsync(p->h_flag_sig, p->d_flag_sig, p->early_n * sizeof(long long), cudaMemcpyDeviceToHost, st));
+        CU(cudaMemcpyAsync(p->h_flag_rel, p->d_flag_rel, p->early_n * (p->prec == TFFT_FP32 ? 4 : 8),
+                           cudaMemcpyDeviceToHost, st));
+    }
+    if (!p->ev_done) CU(cudaEventCreateWithFlags(&p->ev_done, cudaEventDisableTiming));
+    CU(cudaEventRecord(p->ev_done, st));
+    return TFFT_OK;
+}
+
 // Validation, report reset and the fault translated into launch coordinates
 // (shared by the device and the host-streaming entry points).
 int prepare_protected(tfft_plan* p, const void* in, void* out, int64_t batch, int scheme, double delta,
@@ -626,6 +647,9 @@ int tfft_plan_create(tfft_plan** out, int64_t n, int precision, int nstages, con
     }
     if (cudaMalloc(&p->d_cnt, sizeof(Counters)) != cudaSuccess) return cleanup(fail(TFFT_ENOMEM, "counters"));
     if (cudaMallocHost(&p->h_cnt, sizeof(Counters)) != cudaSuccess) return cleanup(fail(TFFT_ENOMEM, "pinned counters"));
+    if (cudaMallocHost(&p->h_flag_sig, tfft_plan::kEarly * sizeof(long long)) != cudaSuccess ||
+        cudaMallocHost(&p->h_flag_rel, tfft_plan::kEarly * sizeof(double)) != cudaSuccess)
+        return cleanup(fail(TFFT_ENOMEM, "pinned flag summary"));
     *out = p;
     return TFFT_OK;
 }
@@ -638,6 +662,8 @@ int tfft_plan_destroy(tfft_plan* p) {
     if (p->have_fast) multi_plan_free(p->fast);
     cudaFree(p->d_cnt);
     cudaFreeHost(p->h_cnt);
+    if (p->h_flag_sig) cudaFreeHost(p->h_flag_sig);
+    if (p->h_flag_rel) cudaFreeHost(p->h_flag_rel);
     cudaFree(p->d_flag_sig);
     cudaFree(p->d_flag_rel);
     cudaFree(p->d_scratch);
@@ -803,9 +829,8 @@ int tfft_protect_launch(tfft_plan* p, const void* in, void* out, int64_t batch, 
     if (rc) return rc;
     if (!prot) return TFFT_OK;
     // the (tiny) detection summary rides back behind the transform
-    CU(cudaMemcpyAsync(p->h_cnt, p->d_cnt, sizeof(Counters), cudaMemcpyDeviceToHost, st));
-    if (!p->ev_done) CU(cudaEventCreateWithFlags(&p->ev_done, cudaEventDisableTiming));
-    CU(cudaEventRecord(p->ev_done, st));
+    rc = enqueue_summary(p, st);
+    if (rc) return rc;
     return TFFT_OK;
 }
 
@@ -863,7 +888,13 @@ int read_summary(tfft_plan* p, int64_t batch, cudaStream_t st, tfft_report* rep,
     }
     flags.clear();
     std::vector<long long> rsig;
-    if (nflag > 0) {
+    if (nflag > 0 && nflag <= p->early_n) {  // already on the host
+        for (int64_t i = 0; i < nflag; ++i) {
+            const double r = p->prec == TFFT_FP32 ? (double)((const float*)p->h_flag_rel)[i] : p->h_flag_rel[i];
+            if (r < 0) rsig.push_back(p->h_flag_sig[i]);
+            else flags.emplace_back(p->h_flag_sig[i], r);
+        }
+    } else if (nflag > 0) {
         std::vector<long long> sig(nflag);
         CU(cudaMemcpyAsync(sig.data(), p->d_flag_sig, nflag * sizeof(long long), cudaMemcpyDeviceToHost, st));
         std::vector<double> rel(nflag);
@@ -945,11 +976,15 @@ int correct_groups(tfft_plan* p, const void* in, void* out, int scheme, const vo
     const int64_t chunk_max = std::max<int64_t>(1, std::min<int64_t>(4096, (int64_t(1) << 28) / (n * (int64_t)p->esize)));
     for (size_t c0 = 0; c0 < fix_groups.size(); c0 += chunk_max) {
         const int64_t K = std::min<int64_t>(chunk_max, fix_groups.size() - c0);
-        rc = ensure_scratch(p, (size_t)3 * K * n * p->esize);
+        const long long chunks = (n + FIX_CHUNK - 1) / FIX_CHUNK;
+        const size_t tb = p->prec == TFFT_FP32 ? 4 : 8;
+        // s0 | W s0 | rebuilt signals | per-chunk checksum partials
+        rc = ensure_scratch(p, (size_t)3 * K * n * p->esize + (size_t)K * chunks * 5 * tb);
         if (rc) return rc;
         char* s0 = (char*)p->d_scratch;
         char* ws0 = s0 + (size_t)K * n * p->esize;
-        char* fx = ws0 + (size_t)K * n * p->esize;
+        char* fx2 = ws0 + (size_t)K * n * p->esize;
+        char* part = fx2 + (size_t)K * n * p->esize;
         if (K > p->jobs_cap) {
             cudaFree(p->d_jobs);
             p->d_jobs = nullptr;
@@ -976,14 +1011,23 @@ int correct_groups(tfft_plan* p, const void* in, void* out, int scheme, const vo
         Launch W = base_launch(s0, ws0, K, inverse ? 1 : 0);
         rc = launch_transform(p, W, st);
         if (rc) return rc;
-        if (p->prec == TFFT_FP32)
-            fix_groups_kernel<float><<<(unsigned)K, AUX_THREADS, 0, st>>>(
-                (const float2*)in, (float2*)out, n, p->bs, (const float2*)ws0, (float2*)fx,
-                (const float2*)etw, (const float2*)values, (float)delta, (float)abs_floor, 1e-6f, p->d_jobs);
-        else
-            fix_groups_kernel<double><<<(unsigned)K, AUX_THREADS, 0, st>>>(
-                (const double2*)in, (double2*)out, n, p->bs, (const double2*)ws0, (double2*)fx,
-                (const double2*)etw, (const double2*)values, delta, abs_floor, 1e-12, p->d_jobs);
+        // rebuild + verify + commit, many CTAs per group (the n points in chunks)
+        const dim3 g((unsigned)chunks, (unsigned)K);
+        if (p->prec == TFFT_FP32) {
+            fix_rebuild_kernel<float><<<g, 256, 0, st>>>((const float2*)in, (const float2*)out, n, p->bs,
+                                                        (const float2*)ws0, (float2*)fx2, (const float2*)etw,
+                                                        (const float2*)values, p->d_jobs, (float*)part);
+            fix_decide_kernel<float><<<(unsigned)K, 32, 0, st>>>(chunks, (const float*)part, (float)delta,
+                                                                (float)abs_floor, 1e-6f, p->d_jobs);
+            fix_commit_kernel<float><<<g, 256, 0, st>>>((float2*)out, n, (const float2*)fx2, p->d_jobs);
+        } else {
+            fix_rebuild_kernel<double><<<g, 256, 0, st>>>((const double2*)in, (const double2*)out, n, p->bs,
+                                                         (const double2*)ws0, (double2*)fx2, (const double2*)etw,
+                                                         (const double2*)values, p->d_jobs, (double*)part);
+            fix_decide_kernel<double><<<(unsigned)K, 32, 0, st>>>(chunks, (const double*)part, delta, abs_floor,
+                                                                 1e-12, p->d_jobs);
+            fix_commit_kernel<double><<<g, 256, 0, st>>>((double2*)out, n, (const double2*)fx2, p->d_jobs);
+        }
         CU(cudaGetLastError());
         CU(cudaMemcpyAsync(jobs.data(), p->d_jobs, K * sizeof(FixJob), cudaMemcpyDeviceToHost, st));
         CU(cudaStreamSynchronize(st));
@@ -1178,8 +1222,8 @@ int tfft_run_protected_host(tfft_plan* p, const void* in, void* out, int64_t bat
     CU(cudaEventRecord(p->ev_out[0], p->s_d2h));
     CU(cudaStreamWaitEvent(st, p->ev_out[0], 0));
     if (!prot) return cudaStreamSynchronize(st) == cudaSuccess ? TFFT_OK : fail(TFFT_ECUDA, "stream sync");
-    CU(cudaMemcpyAsync(p->h_cnt, p->d_cnt, sizeof(Counters), cudaMemcpyDeviceToHost, st));
-    CU(cudaEventRecord(p->ev_done, st));
+    rc = enqueue_summary(p, st);
+    if (rc) return rc;
     CU(cudaStreamSynchronize(st));
     std::vector<std::pair<long long, double>> flags;
     RecheckFn resolve = [&](const std::vector<long long>& sg, std::vector<double>& rr) {
@@ -1304,9 +1348,8 @@ int tfft_run_campaign(tfft_plan* p, const void* in, void* out, int64_t runs, int
     CU(cudaMemsetAsync(p->d_cnt, 0, sizeof(Counters), st));
     rc = launch_transform(p, L, st);
     if (rc) return rc;
-    CU(cudaMemcpyAsync(p->h_cnt, p->d_cnt, sizeof(Counters), cudaMemcpyDeviceToHost, st));
-    if (!p->ev_done) CU(cudaEventCreateWithFlags(&p->ev_done, cudaEventDisableTiming));
-    CU(cudaEventRecord(p->ev_done, st));
+    rc = enqueue_summary(p, st);
+    if (rc) return rc;
     std::vector<std::pair<long long, double>> flags;
     std::vector<std::pair<long long, double>> rechecked;
     RecheckFn resolve = [&](const std::vector<long long>& sg, std::vector<double>& rr) {
@@ -1535,8 +1578,8 @@ int tfft_run_protected_file(tfft_plan* p, const char* in_path, const char* out_p
     if (werr.load()) return fail(werr.load(), werr_msg);
     CU(cudaStreamSynchronize(p->s_d2h));
     if (!prot) return TFFT_OK;
-    CU(cudaMemcpyAsync(p->h_cnt, p->d_cnt, sizeof(Counters), cudaMemcpyDeviceToHost, st));
-    CU(cudaEventRecord(p->ev_done, st));
+    rc = enqueue_summary(p, st);
+    if (rc) return rc;
     std::vector<std::pair<long long, double>> flags;
     RecheckFn resolve = [&](const std::vector<long long>& sg, std::vector<double>& rr) {
         rr.assign(sg.size(), 0.0);
