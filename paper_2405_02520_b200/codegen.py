@@ -309,7 +309,7 @@ PASS_CANDIDATES = {
 # (first, middle, last) variant per log2 L; missing -> (0, 0, 0).
 # Source: tools/tune_pass.py on a B200, ABFT on, 1 GiB (profiles/tune_pass_r01.json).
 PASS_CHOICE = {
-    "fp32": {7: (6, 6, 5), 8: (6, 6, 5), 9: (6, 0, 7), 10: (7, 0, 6), 11: (6, 0, 6)},
+    "fp32": {6: (2, 2, 4), 7: (6, 6, 5), 8: (6, 6, 5), 9: (6, 0, 7), 10: (7, 0, 6), 11: (6, 0, 6)},
     "fp64": {6: (1, 1, 0), 7: (8, 8, 8), 8: (6, 6, 4), 9: (2, 0, 7), 10: (6, 0, 6), 11: (0, 0, 3)},
 }
 

@@ -631,12 +631,12 @@ int tfft_plan_create(tfft_plan** out, int64_t n, int precision, int nstages, con
     } else {
         rc = multi_plan_init(p->multi, n, precision, nstages, dims, p->num_sms);
         if (rc) return cleanup(fail(rc, multi_last_error()));
-        // measured crossover (profiles/sweep_r01_*): fp32 from 2^21, fp64 from 2^19
+        // measured crossover (profiles/sweep_r01_*): fp32 from 2^20, fp64 from 2^19
         static const int fast_env = [] {
             const char* e = getenv("TFFT_FAST3_MIN_LOGN");  // tuning override
             return e ? atoi(e) : 0;
         }();
-        const int fast_min = fast_env ? fast_env : (precision == TFFT_FP32 ? 21 : 19);
+        const int fast_min = fast_env ? fast_env : (precision == TFFT_FP32 ? 20 : 19);
         if (nstages == 2 && p->logn >= fast_min) {
             const int q = p->logn / 3, r = p->logn % 3;  // balanced, larger parts last
             int64_t d3[3];
