@@ -253,69 +253,6 @@ __global__ void fix_commit_kernel(C<T>* __restrict__ out, long long n, const C<T
     for (long long k = k0 + threadIdx.x; k < k1; k += blockDim.x) dst[k] = fx[k];
 }
 
-// Online correction of K flagged groups, one CTA per group:
-//   fixed = W s0 - sum_{b != f} y_b  (pipeline.py:180-185),
-//   then re-verify the rebuilt signal against its input-side checksum and
-//   commit it into `out` only if it passes (protected.py:156-162).
-// ws0: K transformed group sums; scratch: K x n staging.
-template <class T>
-__global__ void __launch_bounds__(AUX_THREADS)
-fix_groups_kernel(const C<T>* __restrict__ in, C<T>* __restrict__ out, long long n, long long bs,
-                  const C<T>* __restrict__ ws0, C<T>* __restrict__ scratch,
-                  const C<T>* __restrict__ etw, const C<T>* __restrict__ values, T delta,
-                  T abs_floor, T floor_coef, FixJob* jobs) {
-    __shared__ T sh[AUX_THREADS / 32];
-    __shared__ int verdict;
-    FixJob job = jobs[blockIdx.x];
-    const C<T>* w = ws0 + (long long)blockIdx.x * n;
-    C<T>* fx = scratch + (long long)blockIdx.x * n;
-    const C<T>* xf = in + job.flagged * n;
-    C<T> cin = mk<T>(T(0), T(0)), cout = mk<T>(T(0), T(0));
-    T l1 = T(0);
-    const T hr = T(-0.5), hi = T(0.8660254037844386467637232);
-    for (long long k = threadIdx.x; k < n; k += blockDim.x) {
-        C<T> others = mk<T>(T(0), T(0));
-        bool first = true;
-        for (long long b = 0; b < bs; ++b) {
-            const long long s = job.first + b;
-            if (s == job.flagged) continue;
-            const C<T> v = out[s * n + k];
-            others = first ? v : cadd<T>(others, v);
-            first = false;
-        }
-        const C<T> f = csub<T>(w[k], others);
-        fx[k] = f;
-        C<T> e;
-        if (values) e = values[k];
-        else {
-            const int cls = (int)(k % 3);
-            e = cls == 0 ? mk<T>(T(1), T(0)) : (cls == 1 ? mk<T>(hr, -hi) : mk<T>(hr, hi));
-        }
-        cout = cadd<T>(cout, cmul<T>(f, e));
-        const C<T> x = xf[k];
-        cin = cadd<T>(cin, cmul<T>(x, etw[k]));
-        l1 = fadd(l1, cabs<T>(x));
-    }
-    T a0 = block_sum(cin.x, sh), a1 = block_sum(cin.y, sh);
-    T a2 = block_sum(cout.x, sh), a3 = block_sum(cout.y, sh);
-    T a4 = block_sum(l1, sh);
-    if (threadIdx.x == 0) {
-        const C<T> raw = mk<T>(fsub(a0, a2), fsub(a1, a3));
-        const T fl = nanmax<T>(abs_floor, fmul(floor_coef, a4));
-        const T den = nanmax<T>(cabs<T>(mk<T>(a0, a1)), fl);
-        T r = cabs<T>(raw) / den;
-        if (!isfinite(r)) r = T(INFINITY);
-        verdict = !(r > delta);
-        jobs[blockIdx.x].ok = verdict;
-    }
-    __syncthreads();
-    if (verdict) {
-        C<T>* dst = out + job.flagged * n;
-        for (long long k = threadIdx.x; k < n; k += blockDim.x) dst[k] = fx[k];
-    }
-}
-
-// out = y_f = ws0 - sum_{b != f} y_b for one signal (tfft_correct_signal).
 template <class T>
 __global__ void rebuild_kernel(const C<T>* __restrict__ ws0, const C<T>* __restrict__ yg,
                                long long bs, long long n, long long f, C<T>* __restrict__ fixed) {

@@ -54,30 +54,6 @@ struct alignas(64) PassArgs {
     long long f_div;
 };
 
-// K block-wide sums in one barrier round (thread 0 gets the totals). The
-// caller guarantees a barrier before `sh` is written again.
-template <int K, class T>
-__device__ __forceinline__ void block_reduce(T (&v)[K], T* sh, int nwarps) {
-#pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) {
-#pragma unroll
-        for (int i = 0; i < K; ++i) v[i] = fadd(v[i], shfl_xor(v[i], off));
-    }
-    if ((threadIdx.x & 31) == 0) {
-#pragma unroll
-        for (int i = 0; i < K; ++i) sh[(threadIdx.x >> 5) * K + i] = v[i];
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-#pragma unroll
-        for (int i = 0; i < K; ++i) {
-            T s = sh[i];
-            for (int w = 1; w < nwarps; ++w) s = fadd(s, sh[w * K + i]);
-            v[i] = s;
-        }
-    }
-}
-
 // element-granular async global->shared copy (SASS LDGSTS)
 template <int BYTES>
 __device__ __forceinline__ void cp_async(void* dst, const void* src) {

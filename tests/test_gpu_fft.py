@@ -90,6 +90,25 @@ def test_ragged_batches_and_host_roundtrip(n, b):
     assert rel_l2(y, np.fft.fft(x.astype(np.complex128))) <= ACC["fp32"] * math.log2(n)
 
 
+@pytest.mark.parametrize("prec,n,b", [("fp32", 32, 5), ("fp32", 32, 70), ("fp64", 32, 3), ("fp32", 64, 9),
+                                      ("fp32", 2048, 3), ("fp32", 4096, 5), ("fp32", 8192, 1),
+                                      ("fp64", 1024, 7), ("fp64", 8192, 2)])
+def test_partial_tiles_of_prefetching_kernels(prec, n, b):
+    """Batches that leave the last CTA tile partly empty (and fewer tiles than
+    CTAs): the tensor-TMA (out-of-bounds rows zero-filled) and in-place
+    prefetch variants, protected and unprotected."""
+    from paper_2405_02520_b200 import Scheme, build_twiddles, make_plan, run_protected
+    from paper_2405_02520_b200.fft_core import fit_group_size
+    rng = np.random.default_rng(n * 7 + b)
+    x = random_batch(rng, (b, n), DT[prec])
+    exact = np.fft.fft(x.astype(np.complex128), axis=-1)
+    plan = fit_group_size(make_plan(n, prec, batch=b), b)
+    for scheme in (Scheme.NONE, Scheme.TWO_SIDED_GROUP):
+        y, rep, _ = run_protected(plan, build_twiddles(plan), torch.from_numpy(x).cuda(), scheme)
+        assert rel_l2(y, exact) <= ACC[prec] * math.log2(n), (prec, n, b, scheme)
+        assert rep.flagged == []
+
+
 def test_device_input_not_mutated():
     for n in (256, 2**16):
         x = torch.randn(4, n, dtype=torch.complex128, device="cuda")
