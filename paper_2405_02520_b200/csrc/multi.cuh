@@ -226,7 +226,10 @@ fft_pass_kernel(const __grid_constant__ PassArgs<T> a) {
             const C<T>* ep = a.etw + ibase + (long long)t * a.in_j;
             const long long es = (long long)TPS * a.in_j;
 #pragma unroll
-            for (int m = 0; m < E; ++m) ew[m] = __ldg(ep + m * es);
+            for (int m = 0; m < E; ++m) {
+                if constexpr (TFFT_ABLATE & 16) ew[m] = mk<T>(T(1), T(0));  // cost attribution only
+                else ew[m] = __ldg(ep + m * es);
+            }
         }
         C<T> v[E];
         if constexpr (BULK) {

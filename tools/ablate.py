@@ -9,7 +9,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def child(logn):
+def child(logn, prec="fp32"):
     sys.path.insert(0, ROOT)
     import torch
     from paper_2405_02520_b200 import _lib, make_plan
@@ -22,12 +22,13 @@ def child(logn):
         if ln == logn:
             _lib.check(lib.tfft_tune_select(0, ln, var))
     n = 1 << logn
-    b = (1 << 30) // (8 * n)
-    x = torch.randn(b * n, dtype=torch.complex64, device="cuda")
+    dt, es = (torch.complex64, 8) if prec == "fp32" else (torch.complex128, 16)
+    b = (1 << 30) // (es * n)
+    x = torch.randn(b * n, dtype=dt, device="cuda")
     y = torch.empty_like(x)
-    plan = fit_group_size(make_plan(n, "fp32", batch=b), b)
+    plan = fit_group_size(make_plan(n, prec, batch=b), b)
     h = native_plan(plan, 0)
-    row = make_encoding("wang", n).device_row(torch.complex64)
+    row = make_encoding("wang", n).device_row(dt)
     rep = _lib.Report()
     sp = torch.cuda.current_stream().cuda_stream
     out = {}
@@ -45,12 +46,12 @@ def child(logn):
                 ts.append(e0.elapsed_time(e1))
         out[sc] = round(sorted(ts)[len(ts) // 2], 4)
     print(json.dumps({"lib": os.path.basename(os.environ.get("TFFT_LIB_PATH", "product")),
-                      "variants": os.environ.get("TFFT_VARIANTS", ""), "n": n, **out}), flush=True)
+                      "variants": os.environ.get("TFFT_VARIANTS", ""), "prec": prec, "n": n, **out}), flush=True)
 
 
 if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "child":
-        child(int(sys.argv[2]))
+        child(int(sys.argv[2]), sys.argv[3] if len(sys.argv) > 3 else "fp32")
     else:
         libs = [None] + sorted(os.path.join(ROOT, "paper_2405_02520_b200", "ablate", f)
                                for f in os.listdir(os.path.join(ROOT, "paper_2405_02520_b200", "ablate")))
@@ -60,5 +61,6 @@ if __name__ == "__main__":
                 env["TFFT_VARIANTS"] = variants
                 if lib:
                     env["TFFT_LIB_PATH"] = lib
-                for logn in (11, 12, 13):
-                    subprocess.run([sys.executable, __file__, "child", str(logn)], env=env)
+                for spec in os.environ.get("ABLATE_SIZES", "fp32:11,fp32:12,fp32:13").split(","):
+                    prec, logn = spec.split(":")
+                    subprocess.run([sys.executable, __file__, "child", logn, prec], env=env)
