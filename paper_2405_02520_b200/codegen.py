@@ -267,13 +267,14 @@ PASS_CANDIDATES = {
         1: _pc((2, (2,), 16, 1, 0)), 2: _pc((4, (4,), 16, 1, 0)), 3: _pc((8, (8,), 16, 1, 0)),
         4: _pc((16, (16,), 16, 1, 0)), 5: _pc((8, (8, 4), 16, 1, 0)),
         6: _pc((8, (8, 8), 16, 1, 0), (8, (8, 8), 32, 2, 3), (8, (8, 8), 16, 3, 3), (8, (8, 8), 32, 2, 2),
-               (8, (8, 8), 16, 3, 2)),
+               (8, (8, 8), 16, 3, 2), (8, (8, 8), 32, 2, 4), (8, (8, 8), 16, 3, 4)),
         7: _pc((16, (16, 8), 16, 1, 0), (16, (16, 8), 16, 2, 1), (16, (16, 8), 8, 3, 1),
                (8, (8, 8, 2), 16, 2, 1), (16, (16, 8), 16, 2, 2), (16, (16, 8), 8, 3, 2),
-               (16, (16, 8), 16, 2, 3), (16, (16, 8), 8, 3, 3), (16, (16, 8), 32, 1, 3)),
+               (16, (16, 8), 16, 2, 3), (16, (16, 8), 8, 3, 3), (16, (16, 8), 32, 1, 3),
+               (16, (16, 8), 16, 2, 4), (16, (16, 8), 8, 3, 4)),
         8: _pc((16, (16, 16), 16, 1, 0), (16, (16, 16), 16, 2, 1), (16, (16, 16), 8, 3, 1),
                (16, (16, 16), 8, 2, 0), (16, (16, 16), 16, 2, 2), (16, (16, 16), 8, 3, 2),
-               (16, (16, 16), 16, 2, 3), (16, (16, 16), 8, 3, 3)),
+               (16, (16, 16), 16, 2, 3), (16, (16, 16), 8, 3, 3), (16, (16, 16), 16, 2, 4)),
         9: _pc((16, (16, 16, 2), 16, 1, 0), (16, (16, 16, 2), 8, 2, 1), (16, (16, 16, 2), 4, 3, 1),
                (16, (16, 16, 2), 8, 2, 0), (16, (16, 16, 2), 8, 2, 2), (16, (16, 16, 2), 16, 1, 2),
                (16, (16, 16, 2), 16, 1, 3), (16, (16, 16, 2), 8, 2, 3)),
@@ -288,13 +289,14 @@ PASS_CANDIDATES = {
         1: _pc((2, (2,), 8, 1, 0)), 2: _pc((4, (4,), 8, 1, 0)), 3: _pc((8, (8,), 8, 1, 0)),
         4: _pc((16, (16,), 8, 1, 0)), 5: _pc((8, (8, 4), 8, 1, 0)),
         6: _pc((8, (8, 8), 8, 1, 0), (8, (8, 8), 16, 2, 3), (8, (8, 8), 8, 3, 3), (8, (8, 8), 16, 2, 2),
-               (8, (8, 8), 8, 3, 2)),
+               (8, (8, 8), 8, 3, 2), (8, (8, 8), 16, 2, 4)),
         7: _pc((16, (16, 8), 8, 1, 0), (16, (16, 8), 8, 2, 1), (16, (16, 8), 4, 3, 1),
                (8, (8, 8, 2), 8, 2, 1), (16, (16, 8), 8, 2, 2), (16, (16, 8), 4, 3, 2),
-               (16, (16, 8), 8, 2, 3), (16, (16, 8), 4, 3, 3), (16, (16, 8), 16, 1, 3)),
+               (16, (16, 8), 8, 2, 3), (16, (16, 8), 4, 3, 3), (16, (16, 8), 16, 1, 3),
+               (16, (16, 8), 16, 1, 4), (16, (16, 8), 8, 2, 4)),
         8: _pc((16, (16, 16), 8, 1, 0), (16, (16, 16), 8, 2, 1), (16, (16, 16), 4, 2, 1),
                (8, (8, 8, 4), 8, 2, 1), (16, (16, 16), 8, 2, 2), (8, (8, 8, 4), 8, 2, 2),
-               (16, (16, 16), 8, 2, 3), (8, (8, 8, 4), 8, 2, 3)),
+               (16, (16, 16), 8, 2, 3), (8, (8, 8, 4), 8, 2, 3), (16, (16, 16), 8, 2, 4)),
         9: _pc((8, (8, 8, 8), 8, 1, 0), (8, (8, 8, 8), 4, 2, 1), (16, (16, 16, 2), 4, 2, 1),
                (8, (8, 8, 8), 8, 1, 1), (8, (8, 8, 8), 8, 1, 2), (8, (8, 8, 8), 4, 2, 2),
                (8, (8, 8, 8), 8, 1, 3), (8, (8, 8, 8), 4, 2, 3)),
@@ -309,8 +311,8 @@ PASS_CANDIDATES = {
 # (first, middle, last) variant per log2 L; missing -> (0, 0, 0).
 # Source: tools/tune_pass.py on a B200, ABFT on, 1 GiB (profiles/tune_pass_r01.json).
 PASS_CHOICE = {
-    "fp32": {6: (2, 2, 4), 7: (6, 6, 5), 8: (6, 6, 5), 9: (6, 0, 7), 10: (7, 0, 6), 11: (6, 0, 6)},
-    "fp64": {6: (1, 1, 0), 7: (8, 8, 8), 8: (6, 6, 4), 9: (2, 0, 7), 10: (6, 0, 6), 11: (0, 0, 3)},
+    "fp32": {6: (6, 2, 4), 7: (9, 9, 5), 8: (6, 6, 5), 9: (6, 0, 7), 10: (7, 0, 6), 11: (6, 0, 6)},
+    "fp64": {6: (5, 5, 0), 7: (8, 8, 8), 8: (6, 6, 6), 9: (2, 0, 5), 10: (6, 0, 6), 11: (0, 0, 3)},
 }
 
 
@@ -363,11 +365,12 @@ def pass_configs():
                 p = best[1]
                 nbuf = 2 if c["pf"] else 1
                 bufe = l * (u + p)
-                if c["pf"] in (2, 3):  # bulk staging: last-kind rows at a padded stride
+                if c["pf"] in (2, 3, 4):  # bulk staging: last-kind rows at a padded stride
                     su = l + 2 if prec == "fp32" else l + 1
                     bufe = max(bufe, u * su)
                 bufe = (bufe + 15) // 16 * 16  # keeps the second buffer 128-byte aligned
-                smem = nbuf * bufe * eb + 3 * (threads // 32 + 1) * (eb // 2)
+                etwe = (l * u + 15) // 16 * 16 if c["pf"] == 4 else 0  # e^T W tiles (first pass)
+                smem = nbuf * bufe * eb + 2 * etwe * eb + 3 * (threads // 32 + 1) * (eb // 2)
                 out.append(dict(prec=prec, logl=logl, l=l, e=e, radices=radices, u=u, p=p,
                                 threads=threads, smem=smem, minb=c["minb"], pf=c["pf"], variant=vi))
     return out

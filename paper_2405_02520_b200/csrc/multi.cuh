@@ -32,7 +32,8 @@ enum { KIND_FIRST = 0, KIND_MID = 1, KIND_LAST = 2 };
 
 template <class T>
 struct alignas(64) PassArgs {
-    CUtensorMap tmap;                 // PF == 3: strided input rows as a 3-D tensor
+    CUtensorMap tmap;                 // PF >= 3: strided input rows as a 3-D tensor
+    CUtensorMap tmap_etw;             // PF == 4, first pass with ABFT: the e^T W row, same geometry
     const C<T>* in;
     C<T>* out;
     long long batch, sig_base, n;
@@ -92,8 +93,12 @@ fft_pass_kernel(const __grid_constant__ PassArgs<T> a) {
     // buffers on two mbarriers. Rows of the last kind land at a padded stride.
     // PF = 3: like 2, but the strided kinds load whole [U x 256] boxes with one
     // tensor-TMA instruction each (thread 0), the last kind keeps bulk rows.
-    constexpr bool BULK = PF == 2 || PF == 3;
-    constexpr bool TENSOR = PF == 3 && KIND != KIND_LAST;
+    // PF = 4: like 3, and the first pass with ABFT also brings its e^T W tile
+    // with tensor TMA (same box geometry, batch 1) into a parallel buffer
+    // instead of one L2 round trip of per-element loads.
+    constexpr bool BULK = PF == 2 || PF == 3 || PF == 4;
+    constexpr bool TENSOR = (PF == 3 || PF == 4) && KIND != KIND_LAST;
+    constexpr bool ETW_TMA = PF == 4 && KIND == KIND_FIRST && ABFT != ABFT_OFF;
     constexpr int BOXR = L < 256 ? L : 256;
     constexpr int SU = sizeof(T) == 4 ? L + 2 : L + 1;  // 16-byte aligned padded row
     // buffer size rounded to 16 elements so the second buffer stays 128-byte
@@ -102,8 +107,10 @@ fft_pass_kernel(const __grid_constant__ PassArgs<T> a) {
     constexpr int ISSUERS = KIND == KIND_LAST ? U : (TENSOR ? 1 : (L < THREADS ? L : THREADS));
     using Eng = Engine<T, L, E, Radices>;
     extern __shared__ __align__(128) unsigned char smem_raw[];
+    constexpr int ETWE = PF == 4 ? (L * U + 15) / 16 * 16 : 0;  // e^T W tile (elements)
     C<T>* tile = reinterpret_cast<C<T>*>(smem_raw);
-    T* red = reinterpret_cast<T*>(tile + (PF ? 2 : 1) * BUFE);
+    C<T>* etile = tile + (PF ? 2 : 1) * BUFE;                   // 2 x ETWE
+    T* red = reinterpret_cast<T*>(etile + 2 * ETWE);
     __shared__ unsigned long long bbar[2];
 
     const int u = threadIdx.x % U;
@@ -153,7 +160,7 @@ fft_pass_kernel(const __grid_constant__ PassArgs<T> a) {
         }
     };
     // bulk variant: the ISSUERS threads each arrive with their byte count
-    auto issue_bulk = [&](long long tx, C<T>* buf, unsigned long long* bar) {
+    auto issue_bulk = [&](long long tx, C<T>* buf, C<T>* ebuf, unsigned long long* bar) {
         if (threadIdx.x >= ISSUERS) return;
         long long bb, ts;
         tile_of(tx, bb, ts);
@@ -163,11 +170,16 @@ fft_pass_kernel(const __grid_constant__ PassArgs<T> a) {
         fence_proxy_async();
         if constexpr (TENSOR) {  // boxes of [U contiguous x BOXR strided rows]
             constexpr int CW = sizeof(C<T>) / 4;  // 32-bit words per element
-            mbar_expect_tx(bar, L * U * sizeof(C<T>));
+            mbar_expect_tx(bar, (ETW_TMA ? 2 : 1) * L * U * sizeof(C<T>));
             const int c2 = KIND == KIND_FIRST ? (int)bb : (int)(bb * (a.n / a.in_hi) + h0);
 #pragma unroll
             for (int k = 0; k < L / BOXR; ++k)
                 tma_load_3d(buf + k * BOXR * U, &a.tmap, (int)(l0 * CW), k * BOXR, c2, bar);
+            if constexpr (ETW_TMA) {
+#pragma unroll
+                for (int k = 0; k < L / BOXR; ++k)
+                    tma_load_3d(ebuf + k * BOXR * U, &a.tmap_etw, (int)(l0 * CW), k * BOXR, 0, bar);
+            }
         } else if constexpr (KIND == KIND_LAST) {  // row u: L contiguous elements
             const unsigned bytes = L * sizeof(C<T>);
             mbar_expect_tx(bar, bytes);
@@ -188,7 +200,7 @@ fft_pass_kernel(const __grid_constant__ PassArgs<T> a) {
             mbar_init(&bbar[1], ISSUERS);
         }
         __syncthreads();
-        if (blockIdx.x < total) issue_bulk(blockIdx.x, tile, &bbar[0]);
+        if (blockIdx.x < total) issue_bulk(blockIdx.x, tile, etile, &bbar[0]);
     } else if constexpr (PF) {
         if (blockIdx.x < total) issue(blockIdx.x, tile);
         cp_async_commit();
@@ -222,7 +234,7 @@ fft_pass_kernel(const __grid_constant__ PassArgs<T> a) {
         // data is waited for so its latency overlaps (one batch of
         // independent loads, not one round trip per element)
         C<T> ew[(KIND == KIND_FIRST && ABFT != ABFT_OFF) ? E : 1];
-        if constexpr (KIND == KIND_FIRST && ABFT != ABFT_OFF) {
+        if constexpr (KIND == KIND_FIRST && ABFT != ABFT_OFF && !ETW_TMA) {
             const C<T>* ep = a.etw + ibase + (long long)t * a.in_j;
             const long long es = (long long)TPS * a.in_j;
 #pragma unroll
@@ -234,7 +246,8 @@ fft_pass_kernel(const __grid_constant__ PassArgs<T> a) {
         C<T> v[E];
         if constexpr (BULK) {
             if (tix + gridDim.x < total)
-                issue_bulk(tix + gridDim.x, (it & 1) ? tile : tile + BUFE, &bbar[(it + 1) & 1]);
+                issue_bulk(tix + gridDim.x, (it & 1) ? tile : tile + BUFE, (it & 1) ? etile : etile + ETWE,
+                           &bbar[(it + 1) & 1]);
             mbar_wait(&bbar[it & 1], (it >> 1) & 1);
             if constexpr (KIND == KIND_LAST) {
 #pragma unroll
@@ -242,6 +255,11 @@ fft_pass_kernel(const __grid_constant__ PassArgs<T> a) {
             } else {
 #pragma unroll
                 for (int m = 0; m < E; ++m) v[m] = cur[(t + m * TPS) * U + u];
+            }
+            if constexpr (ETW_TMA) {
+                const C<T>* ecur = (it & 1) ? etile + ETWE : etile;
+#pragma unroll
+                for (int m = 0; m < E; ++m) ew[m] = ecur[(t + m * TPS) * U + u];
             }
             __syncthreads();
         } else if constexpr (PF) {

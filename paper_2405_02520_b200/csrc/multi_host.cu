@@ -377,9 +377,13 @@ int multi_launch_t(MultiPlan& mp, const MultiLaunch& m, cudaStream_t st) {
             a.f_table = (const FaultRec*)mp.ftab + (size_t)k * m.nfaults;
             a.f_div = m.f_div;
         }
-        if (pe[k]->pf == 3 && kind != KIND_LAST) {
+        if (pe[k]->pf >= 3 && kind != KIND_LAST) {
             int rc = encode_rows_tmap<T>(&a.tmap, a.in, kind, n, m.batch, d0, d1, d2, pe[k]->u, mp.d[k]);
             if (rc) return rc;
+            if (pe[k]->pf == 4 && kind == KIND_FIRST && abft_v != ABFT_OFF) {
+                rc = encode_rows_tmap<T>(&a.tmap_etw, m.etw, kind, n, 1, d0, d1, d2, pe[k]->u, mp.d[k]);
+                if (rc) return rc;
+            }
         }
         int rc = launch_pass<T>(mp, pe[k], kind, abft_v, a, mp.num_sms, st);
         if (rc) return rc;
