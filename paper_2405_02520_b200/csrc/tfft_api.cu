@@ -157,7 +157,8 @@ int prepare_kernel(const void* fn, int threads, int smem, int* blocks_per_sm) {
         *blocks_per_sm = it->second;
         return TFFT_OK;
     }
-    if (smem > 48 * 1024) CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    // opt in always: static + dynamic shared memory may pass 48 KB together
+    CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     int nb = 0;
     CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, threads, smem));
     if (nb < 1) return fail(TFFT_EUNSUPPORTED, "kernel does not fit on an SM");
