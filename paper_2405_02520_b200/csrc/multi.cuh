@@ -409,8 +409,7 @@ struct FinalArgs {
     const T* part_out; long long tiles_out;
     T delta, abs_floor, floor_coef;
     int* flag_count;
-    long long* flag_sig;
-    T* flag_rel;
+    FlagRec* flag_rec;
     long long flag_cap;
     typename KeyT<T>::type* max_key;
     T* rel_out;  // optional per-signal relative discrepancy
@@ -451,8 +450,7 @@ __global__ void __launch_bounds__(256) abft_finalize_kernel(const FinalArgs<T> a
             if (flagged || recheck) {
                 const int slot = atomicAdd(a.flag_count, 1);
                 if (slot < a.flag_cap) {
-                    a.flag_sig[slot] = a.sig_base + b;
-                    a.flag_rel[slot] = rel;
+                    a.flag_rec[slot] = FlagRec{a.sig_base + b, (double)rel};
                 }
             }
         }
@@ -532,8 +530,7 @@ __global__ void __launch_bounds__(256) abft_finalize_cta_kernel(const FinalArgs<
             if (flagged || recheck) {
                 const int slot = atomicAdd(a.flag_count, 1);
                 if (slot < a.flag_cap) {
-                    a.flag_sig[slot] = a.sig_base + b;
-                    a.flag_rel[slot] = rel;
+                    a.flag_rec[slot] = FlagRec{a.sig_base + b, (double)rel};
                 }
             }
         }
@@ -596,8 +593,7 @@ struct MultiLaunch {
     long long f_signal, f_elem;
     int f_where, f_stage, f_comp, f_bit;
     int* flag_count;
-    long long* flag_sig;
-    void* flag_rel;
+    FlagRec* flag_rec;
     long long flag_cap;
     unsigned long long* max_key;
     int only_stage;  // -1: whole transform; k: just stage k, in -> out

@@ -401,8 +401,7 @@ int multi_launch_t(MultiPlan& mp, const MultiLaunch& m, cudaStream_t st) {
         f.abs_floor = (T)m.abs_floor;
         f.floor_coef = sizeof(T) == 4 ? (T)1e-6f : (T)1e-12;
         f.flag_count = m.flag_count;
-        f.flag_sig = m.flag_sig;
-        f.flag_rel = (T*)m.flag_rel;
+        f.flag_rec = m.flag_rec;
         f.flag_cap = m.flag_cap;
         f.max_key = (typename KeyT<T>::type*)m.max_key;
         f.rel_out = (T*)m.rel_out;

@@ -38,6 +38,14 @@ enum { AT_NONE = 0, AT_INPUT = 1, AT_PRESCALE = 2, AT_OUTPUT = 3 };
 // the per-signal threadblock checksums.
 enum { ABFT_OFF = 0, ABFT_WANG = 1, ABFT_TABLE = 2, ABFT_THREAD = 3 };
 
+// One flagged (or recheck) signal: global index and relative discrepancy
+// (double for both precisions). The records follow the counters in one
+// device block, so one copy brings back the counters and the first records.
+struct FlagRec {
+    long long sig;
+    double rel;
+};
+
 template <class T> struct KeyT;
 template <> struct KeyT<float>  { using type = unsigned int; };
 template <> struct KeyT<double> { using type = unsigned long long; };
@@ -75,8 +83,7 @@ struct alignas(64) SingleArgs {
     int scale_inv;          // multiply by 1/N (fft_execute inverse; tile_fft never)
     // results
     int* flag_count;
-    long long* flag_sig;
-    T* flag_rel;
+    FlagRec* flag_rec;
     long long flag_cap;
     typename KeyT<T>::type* max_key;
     T* rel_out;             // optional per-signal relative discrepancy
@@ -332,8 +339,7 @@ fft_single_kernel(const __grid_constant__ SingleArgs<T> a) {
             if (flagged) {
                 const long long slot = base + __popc(ball & ((1u << lane) - 1u));
                 if (slot < a.flag_cap) {
-                    a.flag_sig[slot] = a.sig_base + bsig;
-                    a.flag_rel[slot] = rel;
+                    a.flag_rec[slot] = FlagRec{a.sig_base + bsig, (double)rel};
                 }
             }
         }
@@ -620,8 +626,7 @@ fft_single_kernel(const __grid_constant__ SingleArgs<T> a) {
                 if (flagged) {
                     const long long slot = base + __popc(ball & ((1u << lane) - 1u));
                     if (slot < a.flag_cap) {
-                        a.flag_sig[slot] = a.sig_base + b;
-                        a.flag_rel[slot] = rel;
+                        a.flag_rec[slot] = FlagRec{a.sig_base + b, (double)rel};
                     }
                 }
             }

@@ -106,6 +106,7 @@ struct Counters {
     int pad;
     unsigned long long max_key;  // float key in low 32 bits for fp32
 };
+constexpr size_t kBlockHead = 64;  // Counters, padded: the flag records start 64-byte aligned
 
 // [prec][logn][variant] -> entry, plus the tuned default and a runtime override
 constexpr int kMaxVariants = 16;
@@ -197,11 +198,10 @@ struct tfft_plan {
     // the first kEarly flag entries ride back with the counters (pinned), so a
     // rare fault costs no extra host round trip before the decision
     static constexpr int kEarly = 64;
-    long long* h_flag_sig = nullptr;
-    double* h_flag_rel = nullptr;   // kEarly entries of the plan dtype
+    unsigned char* h_block = nullptr;  // pinned: Counters (64 B) + kEarly FlagRec
     int64_t early_n = 0;
-    long long* d_flag_sig = nullptr;
-    void* d_flag_rel = nullptr;
+    unsigned char* d_block = nullptr;  // device: Counters (64 B) + FlagRec[flag_cap]
+    FlagRec* d_flag_rec = nullptr;
     int64_t flag_cap = 0;
     void* d_scratch = nullptr;      // correction staging
     size_t scratch_bytes = 0;
@@ -225,15 +225,18 @@ struct tfft_plan {
 
 namespace {
 
+// The detection block: counters, then the flag records (capacity >= batch).
 int ensure_flags(tfft_plan* p, int64_t batch) {
-    if (batch <= p->flag_cap) return TFFT_OK;
-    cudaFree(p->d_flag_sig);
-    cudaFree(p->d_flag_rel);
-    p->d_flag_sig = nullptr;
-    p->d_flag_rel = nullptr;
-    CU(cudaMalloc(&p->d_flag_sig, batch * sizeof(long long)));
-    CU(cudaMalloc(&p->d_flag_rel, batch * sizeof(double)));
-    p->flag_cap = batch;
+    if (batch <= p->flag_cap && p->d_block) return TFFT_OK;
+    const int64_t cap = std::max<int64_t>(batch, tfft_plan::kEarly);
+    unsigned char* blk = nullptr;
+    CU(cudaMalloc(&blk, kBlockHead + cap * sizeof(FlagRec)));
+    CU(cudaMemset(blk, 0, kBlockHead));
+    cudaFree(p->d_block);
+    p->d_block = blk;
+    p->d_cnt = reinterpret_cast<Counters*>(blk);
+    p->d_flag_rec = reinterpret_cast<FlagRec*>(blk + kBlockHead);
+    p->flag_cap = cap;
     return TFFT_OK;
 }
 
@@ -319,8 +322,7 @@ int launch_single_t(tfft_plan* p, const Launch& L, cudaStream_t st) {
     a.inverse = L.inverse;
     a.scale_inv = L.scale_inv;
     a.flag_count = &p->d_cnt->flag_count;
-    a.flag_sig = p->d_flag_sig;
-    a.flag_rel = (T*)p->d_flag_rel;
+    a.flag_rec = p->d_flag_rec;
     a.flag_cap = p->flag_cap;
     a.max_key = (typename KeyT<T>::type*)&p->d_cnt->max_key;
     a.rel_out = (T*)L.rel_out;
@@ -358,8 +360,7 @@ int launch_transform(tfft_plan* p, const Launch& L, cudaStream_t st) {
     m.f_signal = L.f_signal; m.f_elem = L.f_elem; m.f_where = L.f_where;
     m.f_stage = L.f_stage; m.f_comp = L.f_comp; m.f_bit = L.f_bit;
     m.flag_count = &p->d_cnt->flag_count;
-    m.flag_sig = p->d_flag_sig;
-    m.flag_rel = p->d_flag_rel;
+    m.flag_rec = p->d_flag_rec;
     m.flag_cap = p->flag_cap;
     m.max_key = &p->d_cnt->max_key;
     m.only_stage = -1;
@@ -495,13 +496,10 @@ int64_t groups_per_chunk(const tfft_plan* p, int64_t batch) {
 // The detection summary behind the kernels: counters plus the first kEarly
 // flag entries (only read on the host when flag_count says so), then ev_done.
 int enqueue_summary(tfft_plan* p, cudaStream_t st) {
-    CU(cudaMemcpyAsync(p->h_cnt, p->d_cnt, sizeof(Counters), cudaMemcpyDeviceToHost, st));
+    // one copy: the counters and the first kEarly flag records
     p->early_n = std::min<int64_t>(tfft_plan::kEarly, p->flag_cap);
-    if (p->early_n > 0) {
-        CU(cudaMemcpyAsync(p->h_flag_sig, p->d_flag_sig, p->early_n * sizeof(long long), cudaMemcpyDeviceToHost, st));
-        CU(cudaMemcpyAsync(p->h_flag_rel, p->d_flag_rel, p->early_n * (p->prec == TFFT_FP32 ? 4 : 8),
-                           cudaMemcpyDeviceToHost, st));
-    }
+    CU(cudaMemcpyAsync(p->h_block, p->d_block, kBlockHead + p->early_n * sizeof(FlagRec), cudaMemcpyDeviceToHost,
+                       st));
     if (!p->ev_done) CU(cudaEventCreateWithFlags(&p->ev_done, cudaEventDisableTiming));
     CU(cudaEventRecord(p->ev_done, st));
     return TFFT_OK;
@@ -646,11 +644,10 @@ int tfft_plan_create(tfft_plan** out, int64_t n, int precision, int nstages, con
             if (!p->have_fast) multi_plan_free(p->fast);
         }
     }
-    if (cudaMalloc(&p->d_cnt, sizeof(Counters)) != cudaSuccess) return cleanup(fail(TFFT_ENOMEM, "counters"));
-    if (cudaMallocHost(&p->h_cnt, sizeof(Counters)) != cudaSuccess) return cleanup(fail(TFFT_ENOMEM, "pinned counters"));
-    if (cudaMallocHost(&p->h_flag_sig, tfft_plan::kEarly * sizeof(long long)) != cudaSuccess ||
-        cudaMallocHost(&p->h_flag_rel, tfft_plan::kEarly * sizeof(double)) != cudaSuccess)
-        return cleanup(fail(TFFT_ENOMEM, "pinned flag summary"));
+    if (ensure_flags(p, tfft_plan::kEarly) != TFFT_OK) return cleanup(TFFT_ENOMEM);
+    if (cudaMallocHost(&p->h_block, kBlockHead + tfft_plan::kEarly * sizeof(FlagRec)) != cudaSuccess)
+        return cleanup(fail(TFFT_ENOMEM, "pinned detection block"));
+    p->h_cnt = reinterpret_cast<Counters*>(p->h_block);
     *out = p;
     return TFFT_OK;
 }
@@ -661,12 +658,8 @@ int tfft_plan_destroy(tfft_plan* p) {
     cudaFree(p->tw);
     multi_plan_free(p->multi);
     if (p->have_fast) multi_plan_free(p->fast);
-    cudaFree(p->d_cnt);
-    cudaFreeHost(p->h_cnt);
-    if (p->h_flag_sig) cudaFreeHost(p->h_flag_sig);
-    if (p->h_flag_rel) cudaFreeHost(p->h_flag_rel);
-    cudaFree(p->d_flag_sig);
-    cudaFree(p->d_flag_rel);
+    cudaFree(p->d_block);
+    if (p->h_block) cudaFreeHost(p->h_block);
     cudaFree(p->d_scratch);
     cudaFree(p->d_jobs);
     cudaFree(p->d_ftab);
@@ -890,24 +883,18 @@ int read_summary(tfft_plan* p, int64_t batch, cudaStream_t st, tfft_report* rep,
     flags.clear();
     std::vector<long long> rsig;
     if (nflag > 0 && nflag <= p->early_n) {  // already on the host
+        const FlagRec* hr = reinterpret_cast<const FlagRec*>(p->h_block + kBlockHead);
         for (int64_t i = 0; i < nflag; ++i) {
-            const double r = p->prec == TFFT_FP32 ? (double)((const float*)p->h_flag_rel)[i] : p->h_flag_rel[i];
-            if (r < 0) rsig.push_back(p->h_flag_sig[i]);
-            else flags.emplace_back(p->h_flag_sig[i], r);
+            if (hr[i].rel < 0) rsig.push_back(hr[i].sig);
+            else flags.emplace_back(hr[i].sig, hr[i].rel);
         }
     } else if (nflag > 0) {
+        std::vector<FlagRec> recs(nflag);
+        CU(cudaMemcpyAsync(recs.data(), p->d_flag_rec, nflag * sizeof(FlagRec), cudaMemcpyDeviceToHost, st));
+        CU(cudaStreamSynchronize(st));
         std::vector<long long> sig(nflag);
-        CU(cudaMemcpyAsync(sig.data(), p->d_flag_sig, nflag * sizeof(long long), cudaMemcpyDeviceToHost, st));
         std::vector<double> rel(nflag);
-        if (p->prec == TFFT_FP32) {
-            std::vector<float> r32(nflag);
-            CU(cudaMemcpyAsync(r32.data(), p->d_flag_rel, nflag * sizeof(float), cudaMemcpyDeviceToHost, st));
-            CU(cudaStreamSynchronize(st));
-            for (int64_t i = 0; i < nflag; ++i) rel[i] = r32[i];
-        } else {
-            CU(cudaMemcpyAsync(rel.data(), p->d_flag_rel, nflag * sizeof(double), cudaMemcpyDeviceToHost, st));
-            CU(cudaStreamSynchronize(st));
-        }
+        for (int64_t i = 0; i < nflag; ++i) { sig[i] = recs[i].sig; rel[i] = recs[i].rel; }
         for (int64_t i = 0; i < nflag; ++i) {
             if (rel[i] < 0) rsig.push_back(sig[i]);
             else flags.emplace_back(sig[i], rel[i]);
