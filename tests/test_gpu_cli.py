@@ -85,3 +85,28 @@ def test_file_stream_matches_device_path(tmp_path, n, prec, batch, scheme):
     assert rep.to_json() == rd.to_json() and cnt.total == cd.total
     if scheme != "none":
         assert [c["signal"] for c in rep.corrected] == [batch - 2]
+
+
+def test_cli_inject_and_bench(tmp_path):
+    """`inject` writes the reference's ROC / records CSV formats and prints the
+    summary JSON; `bench` emits the reference's CSV columns."""
+    roc, rec = tmp_path / "roc.csv", tmp_path / "records.csv"
+    rc, out, _ = _run(["inject", "--runs", "40", "--n", "64", "--batch", "4", "--seed", "3",
+                       "--roc-out", str(roc), "--records-out", str(rec)])
+    assert rc == 0
+    summary = json.loads(out)
+    assert set(summary) == {"runs", "injected", "detected_at_default_delta", "corrected",
+                            "default_delta", "recompute_count"}
+    assert summary["runs"] == 40 and summary["injected"] == 20
+    gold = open(os.path.join(GOLD, "campaign_n64_records.csv")).read().splitlines()
+    mine = rec.read_text().splitlines()
+    assert mine[0] == gold[0] and len(mine) == len(gold)
+    # run ids, injection flags and fault coordinates are the reference's
+    assert [l.split(",")[:5] for l in mine] == [l.split(",")[:5] for l in gold]
+    assert roc.read_text().splitlines()[0] == open(os.path.join(GOLD, "campaign_n64_roc.csv")).read().splitlines()[0]
+    out_csv = tmp_path / "bench.csv"
+    rc, _, _ = _run(["bench", "--n-list", "64", "--batch-list", "16", "--trials", "2", "--out", str(out_csv)])
+    assert rc == 0
+    lines = out_csv.read_text().splitlines()
+    assert lines[0] == "n,batch,scheme,backend,trials,mean_s,stdev_s,pass_count,recompute_count"
+    assert len(lines) == 1 + 3  # none / one_sided / two_sided_group x backend cuda
