@@ -40,10 +40,10 @@ SINGLE_CANDIDATES = {
         5: _cands((8, (8, 4), 256, 1, 1), (8, (8, 4), 256, 1, 0), (16, (16, 2), 256, 1, 1),
                   (32, (32,), 256, 1, 1), (8, (8, 4), 256, 1, 3), (8, (8, 4), 256, 1, 2),
                   (8, (8, 4), 256, 1, 5), (8, (8, 4), 256, 2, 5), (16, (16, 2), 256, 1, 5),
-                  (4, (4, 4, 2), 256, 2, 5)),
+                  (4, (4, 4, 2), 256, 2, 5), (8, (8, 4), 256, 3, 5)),
         6: _cands((8, (8, 8), 256, 1, 1), (8, (8, 8), 256, 1, 0), (16, (16, 4), 256, 1, 1),
                   (16, (16, 4), 256, 1, 0), (8, (8, 8), 256, 1, 3), (8, (8, 8), 256, 1, 2),
-                  (8, (8, 8), 256, 1, 5), (8, (8, 8), 256, 2, 5)),
+                  (8, (8, 8), 256, 1, 5), (8, (8, 8), 256, 2, 5), (8, (8, 8), 256, 3, 5)),
         7: _cands((16, (16, 8), 256, 1, 0), (16, (16, 8), 256, 1, 1), (8, (8, 8, 2), 256, 1, 0),
                   (16, (16, 8), 256, 3, 0), (16, (16, 8), 256, 1, 2)),
         8: _cands((16, (16, 16), 256, 1, 0), (16, (16, 16), 256, 3, 0), (8, (8, 8, 4), 256, 1, 0),
@@ -105,7 +105,7 @@ SINGLE_CANDIDATES = {
 # tuned winners (index into SINGLE_CANDIDATES[prec][logn]); missing -> 0.
 # Source: tools/tune.py on a B200, ABFT on, 1 GiB batches (profiles/tune_r01.json).
 SINGLE_CHOICE = {
-    "fp32": {1: 1, 2: 1, 3: 4, 4: 5, 5: 6, 6: 7, 7: 0, 8: 4, 9: 0, 10: 1, 11: 6, 12: 6, 13: 8},
+    "fp32": {1: 1, 2: 1, 3: 4, 4: 5, 5: 6, 6: 8, 7: 0, 8: 4, 9: 0, 10: 1, 11: 6, 12: 6, 13: 8},
     "fp64": {1: 1, 2: 2, 3: 3, 4: 7, 5: 5, 6: 4, 7: 0, 8: 2, 9: 1, 10: 4, 11: 4, 12: 4, 13: 2},
 }
 ELEM_BYTES = {"fp32": 8, "fp64": 16}
