@@ -87,7 +87,7 @@ SINGLE_CANDIDATES = {
         7: _cands((16, (16, 8), 256, 1, 0), (8, (8, 8, 2), 256, 1, 0), (16, (16, 8), 256, 1, 1),
                   (16, (16, 8), 256, 1, 2)),
         8: _cands((16, (16, 16), 256, 1, 0), (8, (8, 8, 4), 256, 1, 0), (16, (16, 16), 256, 2, 0),
-                  (16, (16, 16), 256, 2, 2)),
+                  (16, (16, 16), 256, 2, 2), (16, (16, 16), 128, 3, 0), (16, (16, 16), 128, 4, 0)),
         9: _cands((8, (8, 8, 8), 256, 1, 0), (16, (16, 16, 2), 256, 1, 0),
                   (8, (8, 8, 8), 256, 3, 0), (8, (8, 8, 8), 256, 3, 2),
                   (8, (8, 8, 8), 256, 2, 4), (16, (16, 16, 2), 128, 2, 0), (16, (16, 16, 2), 128, 3, 0)),
@@ -97,7 +97,7 @@ SINGLE_CANDIDATES = {
                    (16, (16, 16, 4), 128, 2, 0)),
         11: _cands((16, (16, 16, 8), 256, 1, 0), (16, (16, 16, 8), 256, 2, 0),
                    (8, (8, 8, 8, 4), 256, 2, 0), (16, (16, 16, 8), 256, 2, 2),
-                   (8, (8, 8, 8, 4), 256, 2, 4)),
+                   (8, (8, 8, 8, 4), 256, 2, 4), (16, (16, 16, 8), 128, 3, 0), (16, (16, 16, 8), 128, 2, 0)),
         12: _cands((16, (16, 16, 16), 256, 1, 0), (16, (16, 16, 16), 512, 1, 0),
                    (8, (8, 8, 8, 8), 512, 1, 0), (16, (16, 16, 16), 256, 1, 2),
                    (16, (16, 16, 16), 256, 1, 4), (8, (8, 8, 8, 8), 512, 1, 4),
@@ -110,7 +110,7 @@ SINGLE_CANDIDATES = {
 # Source: tools/tune.py on a B200, ABFT on, 1 GiB batches (profiles/tune_r01.json).
 SINGLE_CHOICE = {
     "fp32": {1: 1, 2: 1, 3: 4, 4: 5, 5: 6, 6: 8, 7: 0, 8: 4, 9: 7, 10: 8, 11: 8, 12: 6, 13: 8},
-    "fp64": {1: 1, 2: 2, 3: 3, 4: 7, 5: 5, 6: 4, 7: 0, 8: 2, 9: 6, 10: 4, 11: 4, 12: 4, 13: 2},
+    "fp64": {1: 1, 2: 2, 3: 3, 4: 7, 5: 5, 6: 4, 7: 0, 8: 4, 9: 6, 10: 4, 11: 5, 12: 4, 13: 2},
 }
 ELEM_BYTES = {"fp32": 8, "fp64": 16}
 CTYPE = {"fp32": "float", "fp64": "double"}
