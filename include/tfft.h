@@ -200,10 +200,12 @@ int tfft_encode_group(tfft_plan *plan, const void *xg, int64_t bs, const void *r
                       void *s0, void *s1, void *c_in, void *x_l1, void *stream);
 
 /* abft/pipeline.py:104-135 detect: rel[b] for each of the bs outputs (device
- * real array), NaN/Inf -> +inf. */
+ * real array), NaN/Inf -> +inf. floor_coef is FLOOR_COEF[precision]
+ * (pipeline.py:16,100-101: the caller's `precision` argument, not the data
+ * dtype). */
 int tfft_detect(tfft_plan *plan, const void *yg, int64_t bs, const void *values,
-                const void *c_in, const void *x_l1, double abs_floor, void *rel,
-                void *raw, void *stream);
+                const void *c_in, const void *x_l1, double abs_floor, double floor_coef,
+                void *rel, void *raw, void *stream);
 
 /* abft/pipeline.py:164-192 correct_group core: out[f] = FFT(s0) - sum_{b!=f} y_b
  * computed into `fixed` (n elements). */
@@ -248,6 +250,23 @@ int tfft_tune_select(int precision, int logn, int variant);
  * 1 = middle (3-stage), 2 = last. */
 int tfft_tune_pass_variants(int precision, int logl);
 int tfft_tune_pass_select(int precision, int logl, int kind, int variant);
+
+/* The complete flagged / corrected / unrecoverable lists of the plan's last
+ * protected call (abft/protected.py:35-60 RunReport), for callers whose
+ * report buffers were smaller than the counts that call returned: fills the
+ * lists up to the caps of `report` and sets the three counts. */
+int tfft_report_fetch(const tfft_plan *plan, tfft_report *report);
+
+/* fft_core/reference.py:12-39 dft_reference: direct O(n^2) DFT of `batch`
+ * complex128 device rows of ANY length 1 <= n <= 2^14 (ORACLE_MAX_N),
+ * y_j = sum_k x_k w^(jk), inverse conjugates and scales by 1/n. A kernel of
+ * its own, sharing nothing with the FFT path (the independent check). */
+int tfft_dft(const void *in, void *out, int64_t batch, int64_t n, int inverse, void *stream);
+
+/* Kernels this library has launched in the process so far (every launch
+ * site increments it): bench.py's `gpu_launches` is the difference across
+ * the timed region. */
+int tfft_launch_count(int64_t *count);
 
 const char *tfft_last_error(void);
 int tfft_version(void);

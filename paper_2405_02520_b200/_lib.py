@@ -69,7 +69,7 @@ SIGNATURES = {
     "tfft_plan_exec_passes": (_INT, [_VP]),
     "tfft_tile_fft": (_INT, [_VP, _VP, _I64, _I64, _INT, _INT, _INT, _VP]),
     "tfft_encode_group": (_INT, [_VP, _VP, _I64, _VP, _VP, _VP, _VP, _VP, _VP]),
-    "tfft_detect": (_INT, [_VP, _VP, _I64, _VP, _VP, _VP, _DBL, _VP, _VP, _VP]),
+    "tfft_detect": (_INT, [_VP, _VP, _I64, _VP, _VP, _VP, _DBL, _DBL, _VP, _VP, _VP]),
     "tfft_correct_signal": (_INT, [_VP, _VP, _VP, _I64, _I64, _VP, _INT, _VP]),
     "tfft_element_encode": (_INT, [_INT, _I64, _VP, _VP, _VP, _VP, _VP, _VP, _VP]),
     "tfft_element_verify": (_INT, [_INT, _I64, _VP, _VP, _VP, _VP, _VP, _DBL, _DBL, _VP,
@@ -81,6 +81,9 @@ SIGNATURES = {
     "tfft_tune_select": (_INT, [_INT, _INT, _INT]),
     "tfft_tune_pass_variants": (_INT, [_INT, _INT]),
     "tfft_tune_pass_select": (_INT, [_INT, _INT, _INT, _INT]),
+    "tfft_report_fetch": (_INT, [_VP, ctypes.POINTER(Report)]),
+    "tfft_dft": (_INT, [_VP, _VP, _I64, _I64, _INT, _VP]),
+    "tfft_launch_count": (_INT, [ctypes.POINTER(_I64)]),
     "tfft_last_error": (ctypes.c_char_p, []),
     "tfft_version": (_INT, []),
 }
@@ -127,3 +130,10 @@ def check(rc: int, what: str = ""):
     if rc == TFFT_EIO:
         raise OSError(text)
     raise TfftError(text)
+
+
+def launch_count() -> int:
+    """Kernels libtfft.so has launched in this process (tfft_launch_count)."""
+    c = ctypes.c_int64()
+    check(load().tfft_launch_count(ctypes.byref(c)), "tfft_launch_count")
+    return int(c.value)

@@ -147,9 +147,12 @@ def detect(state: ChecksumState, outputs, enc: EncodingVector, cfg: DetectionCon
     rel = torch.empty(bs, dtype=rdt, device=y.device)
     raw = torch.empty(bs, dtype=y.dtype, device=y.device)
     vals = enc.device_values(y.dtype)
+    if precision not in FLOOR_COEF:
+        raise KeyError(precision)
     _lib.check(lib.tfft_detect(h.handle, y.data_ptr(), bs, _device.ptr(vals),
                                state.c_in.data_ptr(), state.x_l1.data_ptr(), float(cfg.abs_floor),
-                               rel.data_ptr(), raw.data_ptr(), _device.stream_ptr()), "tfft_detect")
+                               FLOOR_COEF[precision], rel.data_ptr(), raw.data_ptr(),
+                               _device.stream_ptr()), "tfft_detect")
     rel_h = rel.cpu().numpy()
     raw_h = raw.cpu().numpy()
     delta = rel_h.dtype.type(cfg.delta)

@@ -100,6 +100,37 @@ def _fault_struct(inj: BitFlipInjector) -> _lib.Fault | None:
     return f
 
 
+def _report_buffers(cap_f, cap_c, cap_u):
+    rep = _lib.Report()
+    flags = (_lib.Flag * max(cap_f, 1))()
+    cg = (ctypes.c_int64 * max(cap_c, 1))()
+    cs = (ctypes.c_int64 * max(cap_c, 1))()
+    ur = (ctypes.c_int64 * max(cap_u, 1))()
+    rep.flagged, rep.flagged_cap = flags, cap_f
+    rep.corrected_group, rep.corrected_signal, rep.corrected_cap = cg, cs, cap_c
+    rep.unrecoverable, rep.unrecoverable_cap = ur, cap_u
+    return rep, (flags, cg, cs, ur)
+
+
+def report_from_native(lib, h, rep, bufs, scheme, delta) -> RunReport:
+    """RunReport of a native call; lists longer than the first buffers (a
+    degenerate batch) are re-read whole with tfft_report_fetch."""
+    if (rep.n_flagged > rep.flagged_cap or rep.n_corrected > rep.corrected_cap
+            or rep.n_unrecoverable > rep.unrecoverable_cap):
+        full, bufs = _report_buffers(rep.n_flagged, rep.n_corrected, rep.n_unrecoverable)
+        _lib.check(lib.tfft_report_fetch(h.handle, ctypes.byref(full)), "tfft_report_fetch")
+    flags, cg, cs, ur = bufs
+    report = RunReport(scheme=scheme.value, delta=delta, groups=int(rep.groups))
+    report.flagged = [{"group": int(flags[i].group), "signal": int(flags[i].signal),
+                       "discrepancy": float(flags[i].discrepancy)} for i in range(rep.n_flagged)]
+    report.corrected = [{"group": int(cg[i]), "signal": int(cs[i])} for i in range(rep.n_corrected)]
+    report.unrecoverable = [int(ur[i]) for i in range(rep.n_unrecoverable)]
+    report.recompute_count = int(rep.recompute_count)
+    report.pass_count = int(rep.pass_count)
+    report.max_rel_discrepancy = float(rep.max_rel_discrepancy)
+    return report
+
+
 def _fused(plan, x, out, scheme, cfg, enc, inverse, injector, host=False):
     """One C-ABI call: tfft_run_protected on device tensors, or (host=True)
     tfft_run_protected_host streaming host tensors through the device."""
@@ -107,15 +138,7 @@ def _fused(plan, x, out, scheme, cfg, enc, inverse, injector, host=False):
     dev = torch.cuda.current_device() if host else x.device.index
     h = native_plan(plan, dev)
     batch = x.shape[0]
-    cap = max(16, min(batch, 1 << 16))
-    flags = (_lib.Flag * cap)()
-    cg = (ctypes.c_int64 * cap)()
-    cs = (ctypes.c_int64 * cap)()
-    ur = (ctypes.c_int64 * cap)()
-    rep = _lib.Report()
-    rep.flagged, rep.flagged_cap = flags, cap
-    rep.corrected_group, rep.corrected_signal, rep.corrected_cap = cg, cs, cap
-    rep.unrecoverable, rep.unrecoverable_cap = ur, cap
+    rep, bufs = _report_buffers(64, 64, 64)
     fault = None
     if injector is not None and not injector.fired:
         fault = _fault_struct(injector)
@@ -126,22 +149,13 @@ def _fused(plan, x, out, scheme, cfg, enc, inverse, injector, host=False):
         vals = enc.device_values(x.dtype)
     entry = lib.tfft_run_protected_host if host else lib.tfft_run_protected
     _lib.check(entry(
-        h.handle, x.data_ptr(), out.data_ptr(), batch, code, float(cfg.delta), float(cfg.abs_floor),
-        _device.ptr(row), _device.ptr(vals), ctypes.byref(fault) if fault is not None else None,
+        h.handle, x.data_ptr() if batch else None, out.data_ptr() if batch else None, batch, code,
+        float(cfg.delta), float(cfg.abs_floor), _device.ptr(row), _device.ptr(vals),
+        ctypes.byref(fault) if fault is not None else None,
         int(bool(inverse)), ctypes.byref(rep), _device.stream_ptr()), "tfft_run_protected")
     if fault is not None and rep.fault_fired:
         injector.fired = True
-    report = RunReport(scheme=scheme.value, delta=cfg.delta, groups=int(rep.groups))
-    if rep.n_flagged > cap or rep.n_corrected > cap or rep.n_unrecoverable > cap:
-        raise RuntimeError("more flagged groups than the report buffers hold")
-    report.flagged = [{"group": int(flags[i].group), "signal": int(flags[i].signal),
-                       "discrepancy": float(flags[i].discrepancy)} for i in range(rep.n_flagged)]
-    report.corrected = [{"group": int(cg[i]), "signal": int(cs[i])} for i in range(rep.n_corrected)]
-    report.unrecoverable = [int(ur[i]) for i in range(rep.n_unrecoverable)]
-    report.recompute_count = int(rep.recompute_count)
-    report.pass_count = int(rep.pass_count)
-    report.max_rel_discrepancy = float(rep.max_rel_discrepancy)
-    return report
+    return report_from_native(lib, h, rep, bufs, scheme, cfg.delta)
 
 
 def _generic(plan, twiddles, x, out, scheme, cfg, enc, inverse, injector, counter):
@@ -236,9 +250,7 @@ def run_protected(plan: FftPlan, twiddles: TwiddleTable, batch, scheme=Scheme.TW
     out = torch.empty_like(x)
     if injector is None or isinstance(injector, BitFlipInjector):
         report = _fused(plan, x, out, scheme, cfg, enc, inverse, injector)
-        nst = len(plan.stages)
         counter = PassCounter(reads=report.pass_count // 2, writes=report.pass_count // 2)
-        del nst
     else:
         counter = PassCounter()
         report = _generic(plan, twiddles, x, out, scheme, cfg, enc, inverse, injector, counter)

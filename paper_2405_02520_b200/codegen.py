@@ -353,12 +353,17 @@ def tile_cost(l, e, radices, u, p, elem_bytes):
     return cost
 
 
-def pass_configs():
+def pass_configs(all_candidates=True):
+    """Every candidate (all_candidates) or only variant 0 (the fallback) and
+    the tuned (first, middle, last) choices per stage dim."""
     out = []
     for prec, table in PASS_CANDIDATES.items():
         eb = ELEM_BYTES[prec]
         for logl, cands in sorted(table.items()):
+            keep = {0, *PASS_CHOICE[prec].get(logl, (0, 0, 0))}
             for vi, c in enumerate(cands):
+                if not all_candidates and vi not in keep:
+                    continue
                 l = 1 << logl
                 e, radices = c["e"], c["radices"]
                 assert math.prod(radices) == l and all(e % r == 0 for r in radices), (prec, logl, c)
@@ -458,8 +463,17 @@ def wang_etw_header():
     return "\n".join(lines) + "\n"
 
 
-def generate(verbose=False):
-    cfgs = single_configs()
+def tuning_build() -> bool:
+    """TFFT_TUNE=1 compiles every tuning candidate (tools/tune*.py); the
+    product build carries only the tuned kernels (+ pass variant 0, the
+    fallback)."""
+    return os.environ.get("TFFT_TUNE", "0") == "1"
+
+
+def generate(verbose=False, all_candidates=None):
+    if all_candidates is None:
+        all_candidates = tuning_build()
+    cfgs = single_configs(all_candidates)
     written = []
     path = os.path.join(CSRC, "wang_etw.cuh")
     _write(path, wang_etw_header())
@@ -478,7 +492,7 @@ def generate(verbose=False):
             path = os.path.join(CSRC, f"gen_single_{prec}_{p}.cu")
             _write(path, _emit_single(prec, part, p))
             written.append(path)
-        pcfgs = [c for c in pass_configs() if c["prec"] == prec]
+        pcfgs = [c for c in pass_configs(all_candidates) if c["prec"] == prec]
         path = os.path.join(CSRC, f"gen_pass_{prec}.cu")
         _write(path, _emit_pass(prec, pcfgs))
         written.append(path)

@@ -413,4 +413,36 @@ element_verify_kernel(int r, long long B, double2* __restrict__ y, const double2
     result[2] = j;
 }
 
+// Direct O(n^2) DFT in complex128 for dft_reference (reference
+// fft_core/reference.py:12-39): y_j = scale * sum_k x_k w^(j k mod n) for ANY
+// length n, w^m from an exactly rounded table. Deliberately shares nothing
+// with the FFT kernels (it is the independent check of the transform path).
+// Grid (ceil(n / 256), batch); the CTA stages 256 inputs at a time in smem.
+__global__ void __launch_bounds__(256)
+dft_direct_kernel(const double2* __restrict__ x, double2* __restrict__ y, long long n,
+                  const double2* __restrict__ w, double scale) {
+    __shared__ double2 xs[256];
+    const long long j = (long long)blockIdx.x * 256 + threadIdx.x;
+    const double2* xb = x + (long long)blockIdx.y * n;
+    double ax = 0.0, ay = 0.0;
+    for (long long k0 = 0; k0 < n; k0 += 256) {
+        __syncthreads();
+        if (k0 + threadIdx.x < n) xs[threadIdx.x] = xb[k0 + threadIdx.x];
+        __syncthreads();
+        if (j < n) {
+            long long e = (j % n) * (k0 % n) % n;  // (j k) mod n, advanced by j per step
+            const int cnt = (int)(n - k0 < 256 ? n - k0 : 256);
+            for (int t = 0; t < cnt; ++t) {
+                const double2 wv = __ldg(w + e);
+                const double2 xv = xs[t];
+                ax = fma(xv.x, wv.x, fma(-xv.y, wv.y, ax));
+                ay = fma(xv.x, wv.y, fma(xv.y, wv.x, ay));
+                e += j;
+                if (e >= n) e -= n;
+            }
+        }
+    }
+    if (j < n) y[(long long)blockIdx.y * n + j] = make_double2(ax * scale, ay * scale);
+}
+
 }  // namespace tfft

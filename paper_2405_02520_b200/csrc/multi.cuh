@@ -411,6 +411,7 @@ struct FinalArgs {
     int* flag_count;
     FlagRec* flag_rec;
     long long flag_cap;
+    unsigned* flag_ovf;
     typename KeyT<T>::type* max_key;
     T* rel_out;  // optional per-signal relative discrepancy
 };
@@ -449,9 +450,7 @@ __global__ void __launch_bounds__(256) abft_finalize_kernel(const FinalArgs<T> a
             if (a.rel_out) a.rel_out[b] = rel;
             if (flagged || recheck) {
                 const int slot = atomicAdd(a.flag_count, 1);
-                if (slot < a.flag_cap) {
-                    a.flag_rec[slot] = FlagRec{a.sig_base + b, (double)rel};
-                }
+                record_flag(a.flag_rec, a.flag_cap, a.flag_ovf, slot, a.sig_base + b, (double)rel);
             }
         }
     }
@@ -529,9 +528,7 @@ __global__ void __launch_bounds__(256) abft_finalize_cta_kernel(const FinalArgs<
             if (a.rel_out) a.rel_out[b] = rel;
             if (flagged || recheck) {
                 const int slot = atomicAdd(a.flag_count, 1);
-                if (slot < a.flag_cap) {
-                    a.flag_rec[slot] = FlagRec{a.sig_base + b, (double)rel};
-                }
+                record_flag(a.flag_rec, a.flag_cap, a.flag_ovf, slot, a.sig_base + b, (double)rel);
             }
         }
         __syncthreads();  // sh reused by the next signal
@@ -595,6 +592,7 @@ struct MultiLaunch {
     int* flag_count;
     FlagRec* flag_rec;
     long long flag_cap;
+    unsigned* flag_ovf;
     unsigned long long* max_key;
     int only_stage;  // -1: whole transform; k: just stage k, in -> out
     const HostFault* faults;  // batched campaign: nfaults runs of f_div signals

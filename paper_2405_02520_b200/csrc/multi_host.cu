@@ -13,6 +13,7 @@
 
 #include "../../include/tfft.h"
 #include "multi.cuh"
+#include "registry.h"
 
 namespace tfft {
 
@@ -241,7 +242,7 @@ int launch_pass(const MultiPlan& mp, const PassEntry* pe, int kind, int abft, Pa
     long long grid = std::min<long long>(total, (long long)nb * num_sms);
     if (grid < 1) grid = 1;
     void* args[] = {&a};
-    MCU(cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(pe->threads), args, pe->smem, st));
+    MCU((tfft::note_launch(), cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(pe->threads), args, pe->smem, st)));
     return TFFT_OK;
 }
 
@@ -403,14 +404,15 @@ int multi_launch_t(MultiPlan& mp, const MultiLaunch& m, cudaStream_t st) {
         f.flag_count = m.flag_count;
         f.flag_rec = m.flag_rec;
         f.flag_cap = m.flag_cap;
+        f.flag_ovf = m.flag_ovf;
         f.max_key = (typename KeyT<T>::type*)m.max_key;
         f.rel_out = (T*)m.rel_out;
         if (tiles[0] >= 1024) {  // few signals, many tiles: a CTA per signal
             const long long grid = std::min<long long>(m.batch, 4LL * mp.num_sms);
-            abft_finalize_cta_kernel<T><<<(unsigned)std::max<long long>(grid, 1), 256, 0, st>>>(f);
+            tfft::note_launch(), abft_finalize_cta_kernel<T><<<(unsigned)std::max<long long>(grid, 1), 256, 0, st>>>(f);
         } else {                 // a warp per signal
             const long long grid = std::min<long long>((m.batch + 7) / 8, 4LL * mp.num_sms);
-            abft_finalize_kernel<T><<<(unsigned)std::max<long long>(grid, 1), 256, 0, st>>>(f);
+            tfft::note_launch(), abft_finalize_kernel<T><<<(unsigned)std::max<long long>(grid, 1), 256, 0, st>>>(f);
         }
         MCU(cudaGetLastError());
     }

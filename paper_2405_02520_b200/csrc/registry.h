@@ -1,7 +1,13 @@
 // Kernel registry filled by the generated instantiation files (codegen.py).
 #pragma once
+#include <atomic>
 
 namespace tfft {
+
+// Kernels this library has launched (process-wide): tfft_launch_count(),
+// the bench's `gpu_launches` claim.
+inline std::atomic<long long> g_launches{0};
+inline void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 struct SingleEntry {
     int logn;

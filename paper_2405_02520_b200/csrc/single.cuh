@@ -46,6 +46,16 @@ struct FlagRec {
     double rel;
 };
 
+// Append one flag: a record while the list has room, else a bit in the
+// overflow mask (the host recomputes those signals' rel exactly). The record
+// list is bounded (kMaxFlagRecords), so a degenerate batch with millions of
+// flags costs batch/8 bytes of mask instead of 16 B per signal.
+__device__ __forceinline__ void record_flag(FlagRec* rec, long long cap, unsigned* ovf, long long slot,
+                                            long long sig, double rel) {
+    if (slot < cap) rec[slot] = FlagRec{sig, rel};
+    else atomicOr(ovf + (sig >> 5), 1u << (sig & 31));
+}
+
 template <class T> struct KeyT;
 template <> struct KeyT<float>  { using type = unsigned int; };
 template <> struct KeyT<double> { using type = unsigned long long; };
@@ -85,6 +95,7 @@ struct alignas(64) SingleArgs {
     int* flag_count;
     FlagRec* flag_rec;
     long long flag_cap;
+    unsigned* flag_ovf;     // bitmask (global signal index) of flags past flag_cap
     typename KeyT<T>::type* max_key;
     T* rel_out;             // optional per-signal relative discrepancy
     // one device-side fault (reference fault_lab/bits.py:56-77 semantics)
@@ -138,7 +149,7 @@ __device__ __forceinline__ void abft_decide(T r0, T r1, T r2, T r3, T l1b, T del
         rel = cabs<T>(mk<T>(dx, dy)) / den;
         if (!isfinite(rel)) rel = T(INFINITY);
         flagged = rel > delta;
-        rel2 = rel * rel;
+        rel2 = T(0);  // the caller keeps exact rel values un-squared
     }
 }
 
@@ -292,7 +303,8 @@ fft_single_kernel(const __grid_constant__ SingleArgs<T> a) {
     const int sl = threadIdx.x / TPS;
     const int t = threadIdx.x % TPS;
     C<T>* sm = sm_all + sl * SL;
-    T my_max = T(0);
+    T my_max = T(0);   // max rel^2 of screen-decided signals
+    T my_maxr = T(0);  // max rel of exactly decided signals (rel^2 would overflow at rel > ~1e19 in fp32)
     if (threadIdx.x == 0) cta_max = 0;
 
     const long long tiles = (a.batch + S - 1) / S;
@@ -325,8 +337,12 @@ fft_single_kernel(const __grid_constant__ SingleArgs<T> a) {
             T rel2;
             abft_decide<T>(sums[0], sums[1], sums[2], sums[3], sums[4], a.delta, a.abs_floor, a.floor_coef,
                            a.rel_out != nullptr, rel, rel2, flagged, recheck);
-            if (recheck) rel = T(-1);  // sentinel: the host recomputes it exactly
-            else my_max = my_max > rel2 ? my_max : rel2;  // squared; sqrt once per CTA
+            if (recheck) {
+                rel = T(-1);  // sentinel: the host recomputes it exactly
+            } else {
+                my_max = my_max > rel2 ? my_max : rel2;  // squared screen value; sqrt once per CTA
+                my_maxr = my_maxr > rel ? my_maxr : rel;  // exact path (rel2 = 0 there: no overflow)
+            }
             if (a.rel_out) a.rel_out[bsig] = rel;
             flagged = flagged || recheck;
         }
@@ -338,9 +354,7 @@ fft_single_kernel(const __grid_constant__ SingleArgs<T> a) {
             base = __shfl_sync(0xffffffffu, base, __ffs(ball) - 1);
             if (flagged) {
                 const long long slot = base + __popc(ball & ((1u << lane) - 1u));
-                if (slot < a.flag_cap) {
-                    a.flag_rec[slot] = FlagRec{a.sig_base + bsig, (double)rel};
-                }
+                record_flag(a.flag_rec, a.flag_cap, a.flag_ovf, slot, a.sig_base + bsig, (double)rel);
             }
         }
     };
@@ -613,8 +627,7 @@ fft_single_kernel(const __grid_constant__ SingleArgs<T> a) {
                 rel = (w != w) ? T(INFINITY) : sqrt(w);
                 if (!isfinite(rel)) rel = T(INFINITY);
                 flagged = rel > a.delta;
-                const T r2 = rel * rel;
-                my_max = my_max > r2 ? my_max : r2;
+                my_maxr = my_maxr > rel ? my_maxr : rel;
                 if (a.rel_out) a.rel_out[b] = rel;
             }
             const unsigned ball = __ballot_sync(0xffffffffu, flagged);
@@ -625,9 +638,7 @@ fft_single_kernel(const __grid_constant__ SingleArgs<T> a) {
                 base = __shfl_sync(0xffffffffu, base, __ffs(ball) - 1);
                 if (flagged) {
                     const long long slot = base + __popc(ball & ((1u << lane) - 1u));
-                    if (slot < a.flag_cap) {
-                        a.flag_rec[slot] = FlagRec{a.sig_base + b, (double)rel};
-                    }
+                    record_flag(a.flag_rec, a.flag_cap, a.flag_ovf, slot, a.sig_base + b, (double)rel);
                 }
             }
         }
@@ -697,7 +708,8 @@ fft_single_kernel(const __grid_constant__ SingleArgs<T> a) {
     }
     if constexpr (ABFT != ABFT_OFF) {
         // one atomic per CTA for the running max discrepancy
-        typename KeyT<T>::type k = order_key(sqrt(my_max));
+        const T mr = sqrt(my_max);
+        typename KeyT<T>::type k = order_key(my_maxr > mr ? my_maxr : mr);
 #pragma unroll
         for (int off = 16; off >= 1; off >>= 1) {
             typename KeyT<T>::type o = __shfl_xor_sync(0xffffffffu, k, off);

@@ -202,7 +202,13 @@ struct tfft_plan {
     int64_t early_n = 0;
     unsigned char* d_block = nullptr;  // device: Counters (64 B) + FlagRec[flag_cap]
     FlagRec* d_flag_rec = nullptr;
-    int64_t flag_cap = 0;
+    int64_t flag_cap = 0;           // records (bounded by kMaxFlagRecords)
+    unsigned* d_ovf = nullptr;      // overflow bitmask, one bit per signal of the batch (zero between calls)
+    int64_t ovf_bits = 0;
+    // the last protected call's complete lists (tfft_report_fetch)
+    std::vector<tfft_flag> last_flagged;
+    std::vector<std::pair<int64_t, int64_t>> last_corrected;
+    std::vector<int64_t> last_unrec;
     void* d_scratch = nullptr;      // correction staging
     size_t scratch_bytes = 0;
     FixJob* d_jobs = nullptr;
@@ -225,18 +231,31 @@ struct tfft_plan {
 
 namespace {
 
-// The detection block: counters, then the flag records (capacity >= batch).
+// The detection block: counters, then up to kMaxFlagRecords flag records;
+// flags past that land in a per-signal overflow bitmask (batch / 8 bytes,
+// written only in that degenerate case and cleared by read_summary).
+constexpr int64_t kMaxFlagRecords = int64_t(1) << 16;
 int ensure_flags(tfft_plan* p, int64_t batch) {
-    if (batch <= p->flag_cap && p->d_block) return TFFT_OK;
-    const int64_t cap = std::max<int64_t>(batch, tfft_plan::kEarly);
-    unsigned char* blk = nullptr;
-    CU(cudaMalloc(&blk, kBlockHead + cap * sizeof(FlagRec)));
-    CU(cudaMemset(blk, 0, kBlockHead));
-    cudaFree(p->d_block);
-    p->d_block = blk;
-    p->d_cnt = reinterpret_cast<Counters*>(blk);
-    p->d_flag_rec = reinterpret_cast<FlagRec*>(blk + kBlockHead);
-    p->flag_cap = cap;
+    const int64_t cap = std::max<int64_t>(std::min<int64_t>(batch, kMaxFlagRecords), tfft_plan::kEarly);
+    if (cap > p->flag_cap || !p->d_block) {
+        unsigned char* blk = nullptr;
+        CU(cudaMalloc(&blk, kBlockHead + cap * sizeof(FlagRec)));
+        CU(cudaMemset(blk, 0, kBlockHead));
+        cudaFree(p->d_block);
+        p->d_block = blk;
+        p->d_cnt = reinterpret_cast<Counters*>(blk);
+        p->d_flag_rec = reinterpret_cast<FlagRec*>(blk + kBlockHead);
+        p->flag_cap = cap;
+    }
+    if (batch > p->flag_cap && batch > p->ovf_bits) {
+        const int64_t bits = (batch + 31) / 32 * 32;
+        unsigned* m = nullptr;
+        CU(cudaMalloc(&m, bits / 8));
+        CU(cudaMemset(m, 0, bits / 8));
+        cudaFree(p->d_ovf);
+        p->d_ovf = m;
+        p->ovf_bits = bits;
+    }
     return TFFT_OK;
 }
 
@@ -324,6 +343,7 @@ int launch_single_t(tfft_plan* p, const Launch& L, cudaStream_t st) {
     a.flag_count = &p->d_cnt->flag_count;
     a.flag_rec = p->d_flag_rec;
     a.flag_cap = p->flag_cap;
+    a.flag_ovf = p->d_ovf;
     a.max_key = (typename KeyT<T>::type*)&p->d_cnt->max_key;
     a.rel_out = (T*)L.rel_out;
     a.f_table = L.f_table;
@@ -342,7 +362,7 @@ int launch_single_t(tfft_plan* p, const Launch& L, cudaStream_t st) {
     long long grid = std::min<long long>(tiles, (long long)nb * p->num_sms);
     if (grid < 1) grid = 1;
     void* args[] = {&a};
-    CU(cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(e->threads), args, e->smem, st));
+    CU((tfft::note_launch(), cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(e->threads), args, e->smem, st)));
     return TFFT_OK;
 }
 
@@ -362,6 +382,7 @@ int launch_transform(tfft_plan* p, const Launch& L, cudaStream_t st) {
     m.flag_count = &p->d_cnt->flag_count;
     m.flag_rec = p->d_flag_rec;
     m.flag_cap = p->flag_cap;
+    m.flag_ovf = p->d_ovf;
     m.max_key = &p->d_cnt->max_key;
     m.only_stage = -1;
     m.faults = L.faults;
@@ -511,7 +532,7 @@ int prepare_protected(tfft_plan* p, const void* in, void* out, int64_t batch, in
                       const void* etw, const void* values, double abs_floor, const tfft_fault* fault, int inverse,
                       tfft_report* rep, Launch& L) {
     if (!rep) return fail(TFFT_EINVAL, "null report");
-    if (batch < 1 || !in || !out) return fail(TFFT_EINVAL, "batch must have shape (B, n) with n == plan.n");
+    if (batch < 0 || (batch > 0 && (!in || !out))) return fail(TFFT_EINVAL, "batch must have shape (B, n) with n == plan.n");
     if (batch % p->bs) return fail(TFFT_EINVAL, "batch size not divisible by group size");
     if (scheme < TFFT_SCHEME_NONE || scheme > TFFT_SCHEME_TWO_SIDED_GROUP) return fail(TFFT_EINVAL, "bad scheme");
     const bool prot = scheme != TFFT_SCHEME_NONE;
@@ -524,6 +545,9 @@ int prepare_protected(tfft_plan* p, const void* in, void* out, int64_t batch, in
     rep->max_rel_discrepancy = 0.0;
     rep->n_flagged = rep->n_corrected = rep->n_unrecoverable = 0;
     rep->fault_fired = 0;
+    p->last_flagged.clear();
+    p->last_corrected.clear();
+    p->last_unrec.clear();
 
     L = base_launch(in, out, batch, inverse ? 1 : 0);
     L.abft = prot ? (values ? ABFT_TABLE : (p->check_level ? ABFT_THREAD : ABFT_WANG)) : ABFT_OFF;
@@ -659,6 +683,7 @@ int tfft_plan_destroy(tfft_plan* p) {
     multi_plan_free(p->multi);
     if (p->have_fast) multi_plan_free(p->fast);
     cudaFree(p->d_block);
+    cudaFree(p->d_ovf);
     if (p->h_block) cudaFreeHost(p->h_block);
     cudaFree(p->d_scratch);
     cudaFree(p->d_jobs);
@@ -711,9 +736,9 @@ int tfft_scale(void* buf, int64_t count, int dtype_bytes, double s, void* stream
     if (count == 0) return TFFT_OK;
     const int grid = (int)std::min<long long>((count + 255) / 256, 1 << 16);
     if (dtype_bytes == 8)
-        scale_kernel<float><<<grid, 256, 0, (cudaStream_t)stream>>>((float2*)buf, count, (float)s);
+        tfft::note_launch(), scale_kernel<float><<<grid, 256, 0, (cudaStream_t)stream>>>((float2*)buf, count, (float)s);
     else
-        scale_kernel<double><<<grid, 256, 0, (cudaStream_t)stream>>>((double2*)buf, count, s);
+        tfft::note_launch(), scale_kernel<double><<<grid, 256, 0, (cudaStream_t)stream>>>((double2*)buf, count, s);
     CU(cudaGetLastError());
     return TFFT_OK;
 }
@@ -723,7 +748,7 @@ int tfft_flip_bit(void* buf, int64_t word, int bit, int dtype_bytes, void* strea
     const int wbytes = dtype_bytes / 2;
     if (wbytes != 4 && wbytes != 8) return fail(TFFT_EINVAL, "dtype must be complex64/complex128");
     if (bit < 0 || bit >= wbytes * 8) return fail(TFFT_EINVAL, "bit out of range");
-    flip_word_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(buf, word, bit, wbytes);
+    tfft::note_launch(), flip_word_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(buf, word, bit, wbytes);
     CU(cudaGetLastError());
     return TFFT_OK;
 }
@@ -738,17 +763,17 @@ int tfft_encode_group(tfft_plan* p, const void* xg, int64_t bs, const void* row,
     if (s0 || s1) {
         int grid = (int)std::min<long long>((n + 255) / 256, 4LL * p->num_sms);
         if (p->prec == TFFT_FP32)
-            group_sums_kernel<float><<<grid, 256, 0, st>>>((const float2*)xg, bs, n, (float2*)s0, (double2*)s1);
+            tfft::note_launch(), group_sums_kernel<float><<<grid, 256, 0, st>>>((const float2*)xg, bs, n, (float2*)s0, (double2*)s1);
         else
-            group_sums_kernel<double><<<grid, 256, 0, st>>>((const double2*)xg, bs, n, (double2*)s0, (double2*)s1);
+            tfft::note_launch(), group_sums_kernel<double><<<grid, 256, 0, st>>>((const double2*)xg, bs, n, (double2*)s0, (double2*)s1);
         CU(cudaGetLastError());
     }
     if (c_in || x_l1) {
         if (p->prec == TFFT_FP32)
-            dot_l1_kernel<float><<<(unsigned)bs, AUX_THREADS, 0, st>>>((const float2*)xg, n, (const float2*)row,
+            tfft::note_launch(), dot_l1_kernel<float><<<(unsigned)bs, AUX_THREADS, 0, st>>>((const float2*)xg, n, (const float2*)row,
                                                                        (float2*)c_in, (float*)x_l1);
         else
-            dot_l1_kernel<double><<<(unsigned)bs, AUX_THREADS, 0, st>>>((const double2*)xg, n, (const double2*)row,
+            tfft::note_launch(), dot_l1_kernel<double><<<(unsigned)bs, AUX_THREADS, 0, st>>>((const double2*)xg, n, (const double2*)row,
                                                                         (double2*)c_in, (double*)x_l1);
         CU(cudaGetLastError());
     }
@@ -756,19 +781,20 @@ int tfft_encode_group(tfft_plan* p, const void* xg, int64_t bs, const void* row,
 }
 
 int tfft_detect(tfft_plan* p, const void* yg, int64_t bs, const void* values, const void* c_in,
-                const void* x_l1, double abs_floor, void* rel, void* raw, void* stream) {
+                const void* x_l1, double abs_floor, double floor_coef, void* rel, void* raw, void* stream) {
     int rc = check_plan(p);
     if (rc) return rc;
     if (!yg || !c_in || !x_l1 || !rel || bs < 1) return fail(TFFT_EINVAL, "bad buffers");
+    if (!(floor_coef >= 0)) return fail(TFFT_EINVAL, "floor_coef must be >= 0");
     cudaStream_t st = (cudaStream_t)stream;
     if (p->prec == TFFT_FP32)
-        detect_kernel<float><<<(unsigned)bs, AUX_THREADS, 0, st>>>(
+        tfft::note_launch(), detect_kernel<float><<<(unsigned)bs, AUX_THREADS, 0, st>>>(
             (const float2*)yg, p->n, (const float2*)values, (const float2*)c_in, (const float*)x_l1,
-            (float)abs_floor, 1e-6f, (float*)rel, (float2*)raw);
+            (float)abs_floor, (float)floor_coef, (float*)rel, (float2*)raw);
     else
-        detect_kernel<double><<<(unsigned)bs, AUX_THREADS, 0, st>>>(
+        tfft::note_launch(), detect_kernel<double><<<(unsigned)bs, AUX_THREADS, 0, st>>>(
             (const double2*)yg, p->n, (const double2*)values, (const double2*)c_in, (const double*)x_l1,
-            abs_floor, 1e-12, (double*)rel, (double2*)raw);
+            abs_floor, floor_coef, (double*)rel, (double2*)raw);
     CU(cudaGetLastError());
     return TFFT_OK;
 }
@@ -786,10 +812,10 @@ int tfft_correct_signal(tfft_plan* p, const void* s0, const void* yg, int64_t bs
     if (rc) return rc;
     int grid = (int)std::min<long long>((p->n + 255) / 256, 4LL * p->num_sms);
     if (p->prec == TFFT_FP32)
-        rebuild_kernel<float><<<grid, 256, 0, st>>>((const float2*)p->d_scratch, (const float2*)yg, bs, p->n, f,
+        tfft::note_launch(), rebuild_kernel<float><<<grid, 256, 0, st>>>((const float2*)p->d_scratch, (const float2*)yg, bs, p->n, f,
                                                     (float2*)fixed);
     else
-        rebuild_kernel<double><<<grid, 256, 0, st>>>((const double2*)p->d_scratch, (const double2*)yg, bs, p->n,
+        tfft::note_launch(), rebuild_kernel<double><<<grid, 256, 0, st>>>((const double2*)p->d_scratch, (const double2*)yg, bs, p->n,
                                                      f, (double2*)fixed);
     CU(cudaGetLastError());
     return TFFT_OK;
@@ -813,6 +839,7 @@ int tfft_protect_launch(tfft_plan* p, const void* in, void* out, int64_t batch, 
     Launch L;
     rc = prepare_protected(p, in, out, batch, scheme, delta, etw, values, abs_floor, fault, inverse, rep, L);
     if (rc) return rc;
+    if (batch == 0) return TFFT_OK;  // an empty shard: empty report, nothing launched
     const bool prot = scheme != TFFT_SCHEME_NONE;
     if (prot) {
         rc = ensure_flags(p, batch);
@@ -846,16 +873,52 @@ int recheck_device(tfft_plan* p, const void* in, const void* out, const std::vec
     double* d_rel = (double*)(d_sig + k);
     CU(cudaMemcpyAsync(d_sig, sigs.data(), k * sizeof(long long), cudaMemcpyHostToDevice, st));
     if (p->prec == TFFT_FP32)
-        recheck_kernel<float><<<(unsigned)k, AUX_THREADS, 0, st>>>(
+        tfft::note_launch(), recheck_kernel<float><<<(unsigned)k, AUX_THREADS, 0, st>>>(
             (const float2*)in, (const float2*)out, p->n, d_sig, (const float2*)etw, (const float2*)values,
             (float)abs_floor, 1e-6f, d_rel);
     else
-        recheck_kernel<double><<<(unsigned)k, AUX_THREADS, 0, st>>>(
+        tfft::note_launch(), recheck_kernel<double><<<(unsigned)k, AUX_THREADS, 0, st>>>(
             (const double2*)in, (const double2*)out, p->n, d_sig, (const double2*)etw, (const double2*)values,
             abs_floor, 1e-12, d_rel);
     CU(cudaGetLastError());
     CU(cudaMemcpyAsync(rel.data(), d_rel, k * sizeof(double), cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));
+    return TFFT_OK;
+}
+
+// Exact rel of host-resident signals `sg` (sorted global indices), staged
+// through ring slot 0 in runs of consecutive signals (an all-zero batch flags
+// every signal: one copy per run, one recheck launch per slot fill).
+// `stage(first, count, din, dout)` copies the input / output rows of signals
+// [first, first + count) into the device slot.
+using StageFn = std::function<int(int64_t, int64_t, char*, char*)>;
+int recheck_staged(tfft_plan* p, const std::vector<long long>& sg, std::vector<double>& rr, const void* etw,
+                   const void* values, double abs_floor, const StageFn& stage, cudaStream_t st) {
+    rr.assign(sg.size(), 0.0);
+    const size_t sig_bytes = (size_t)p->n * p->esize;
+    const int64_t cap = std::max<int64_t>(1, (int64_t)(p->ring_chunk / sig_bytes));
+    char* din = (char*)p->ring;
+    char* dout = din + p->ring_chunk;
+    size_t i = 0;
+    while (i < sg.size()) {
+        std::vector<long long> local;
+        const size_t i0 = i;
+        int64_t used = 0;
+        while (i < sg.size() && used < cap) {
+            size_t j = i + 1;
+            while (j < sg.size() && sg[j] == sg[j - 1] + 1 && used + (int64_t)(j - i) < cap) ++j;
+            const int64_t cnt = (int64_t)(j - i);
+            int rc = stage(sg[i], cnt, din + used * sig_bytes, dout + used * sig_bytes);
+            if (rc) return rc;
+            for (int64_t k = 0; k < cnt; ++k) local.push_back(used + k);
+            used += cnt;
+            i = j;
+        }
+        std::vector<double> r;
+        int rc = recheck_device(p, din, dout, local, etw, values, abs_floor, r, st);
+        if (rc) return rc;
+        for (size_t k = 0; k < r.size(); ++k) rr[i0 + k] = r[k];
+    }
     return TFFT_OK;
 }
 
@@ -870,7 +933,8 @@ int read_summary(tfft_plan* p, int64_t batch, cudaStream_t st, tfft_report* rep,
                  std::vector<std::pair<long long, double>>& flags, double delta, const RecheckFn& resolve,
                  std::vector<std::pair<long long, double>>* rechecked = nullptr) {
     CU(cudaEventSynchronize(p->ev_done));
-    const int64_t nflag = std::min<int64_t>(p->h_cnt->flag_count, batch);
+    const int64_t ntotal = std::min<int64_t>(p->h_cnt->flag_count, batch);
+    const int64_t nflag = std::min<int64_t>(ntotal, p->flag_cap);
     double max_rel;
     if (p->prec == TFFT_FP32) {
         unsigned int k = (unsigned int)(p->h_cnt->max_key & 0xffffffffull);
@@ -900,6 +964,15 @@ int read_summary(tfft_plan* p, int64_t batch, cudaStream_t st, tfft_report* rep,
             else flags.emplace_back(sig[i], rel[i]);
         }
     }
+    if (ntotal > nflag) {  // degenerate batch: the rest are bits of the overflow mask
+        const int64_t words = (batch + 31) / 32;
+        std::vector<unsigned> mask(words);
+        CU(cudaMemcpyAsync(mask.data(), p->d_ovf, words * sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+        CU(cudaMemsetAsync(p->d_ovf, 0, words * sizeof(unsigned), st));
+        CU(cudaStreamSynchronize(st));
+        for (int64_t w = 0; w < words; ++w)
+            for (unsigned m = mask[w]; m; m &= m - 1) rsig.push_back(w * 32 + __builtin_ctz(m));
+    }
     if (!rsig.empty()) {
         std::sort(rsig.begin(), rsig.end());
         std::vector<double> rr;
@@ -917,10 +990,13 @@ int read_summary(tfft_plan* p, int64_t batch, cudaStream_t st, tfft_report* rep,
     rep->max_rel_discrepancy = max_rel;
     // flagged list, in (group, signal) order like the reference's loop
     rep->n_flagged = (int64_t)flags.size();
-    for (size_t i = 0; i < flags.size() && (int64_t)i < rep->flagged_cap; ++i) {
-        rep->flagged[i].group = flags[i].first / p->bs;
-        rep->flagged[i].signal = flags[i].first;
-        rep->flagged[i].discrepancy = flags[i].second;
+    p->last_flagged.resize(flags.size());
+    for (size_t i = 0; i < flags.size(); ++i) {
+        tfft_flag& f = p->last_flagged[i];
+        f.group = flags[i].first / p->bs;
+        f.signal = flags[i].first;
+        f.discrepancy = flags[i].second;
+        if ((int64_t)i < rep->flagged_cap) rep->flagged[i] = f;
     }
     return TFFT_OK;
 }
@@ -990,10 +1066,10 @@ int correct_groups(tfft_plan* p, const void* in, void* out, int scheme, const vo
         const unsigned gx = (unsigned)std::max<long long>(1, std::min<long long>((n + 255) / 256,
                                                                                (4LL * p->num_sms + K - 1) / K));
         if (p->prec == TFFT_FP32)
-            group_sums_jobs_kernel<float><<<dim3(gx, (unsigned)K), 256, 0, st>>>((const float2*)in, p->bs, n,
+            tfft::note_launch(), group_sums_jobs_kernel<float><<<dim3(gx, (unsigned)K), 256, 0, st>>>((const float2*)in, p->bs, n,
                                                                                 p->d_jobs, (float2*)s0);
         else
-            group_sums_jobs_kernel<double><<<dim3(gx, (unsigned)K), 256, 0, st>>>((const double2*)in, p->bs, n,
+            tfft::note_launch(), group_sums_jobs_kernel<double><<<dim3(gx, (unsigned)K), 256, 0, st>>>((const double2*)in, p->bs, n,
                                                                                  p->d_jobs, (double2*)s0);
         CU(cudaGetLastError());
         Launch W = base_launch(s0, ws0, K, inverse ? 1 : 0);
@@ -1002,19 +1078,19 @@ int correct_groups(tfft_plan* p, const void* in, void* out, int scheme, const vo
         // rebuild + verify + commit, many CTAs per group (the n points in chunks)
         const dim3 g((unsigned)chunks, (unsigned)K);
         if (p->prec == TFFT_FP32) {
-            fix_rebuild_kernel<float><<<g, 256, 0, st>>>((const float2*)in, (const float2*)out, n, p->bs,
+            tfft::note_launch(), fix_rebuild_kernel<float><<<g, 256, 0, st>>>((const float2*)in, (const float2*)out, n, p->bs,
                                                         (const float2*)ws0, (float2*)fx2, (const float2*)etw,
                                                         (const float2*)values, p->d_jobs, (float*)part);
-            fix_decide_kernel<float><<<(unsigned)K, 32, 0, st>>>(chunks, (const float*)part, (float)delta,
+            tfft::note_launch(), fix_decide_kernel<float><<<(unsigned)K, 32, 0, st>>>(chunks, (const float*)part, (float)delta,
                                                                 (float)abs_floor, 1e-6f, p->d_jobs);
-            fix_commit_kernel<float><<<g, 256, 0, st>>>((float2*)out, n, (const float2*)fx2, p->d_jobs);
+            tfft::note_launch(), fix_commit_kernel<float><<<g, 256, 0, st>>>((float2*)out, n, (const float2*)fx2, p->d_jobs);
         } else {
-            fix_rebuild_kernel<double><<<g, 256, 0, st>>>((const double2*)in, (const double2*)out, n, p->bs,
+            tfft::note_launch(), fix_rebuild_kernel<double><<<g, 256, 0, st>>>((const double2*)in, (const double2*)out, n, p->bs,
                                                          (const double2*)ws0, (double2*)fx2, (const double2*)etw,
                                                          (const double2*)values, p->d_jobs, (double*)part);
-            fix_decide_kernel<double><<<(unsigned)K, 32, 0, st>>>(chunks, (const double*)part, delta, abs_floor,
+            tfft::note_launch(), fix_decide_kernel<double><<<(unsigned)K, 32, 0, st>>>(chunks, (const double*)part, delta, abs_floor,
                                                                  1e-12, p->d_jobs);
-            fix_commit_kernel<double><<<g, 256, 0, st>>>((double2*)out, n, (const double2*)fx2, p->d_jobs);
+            tfft::note_launch(), fix_commit_kernel<double><<<g, 256, 0, st>>>((double2*)out, n, (const double2*)fx2, p->d_jobs);
         }
         CU(cudaGetLastError());
         CU(cudaMemcpyAsync(jobs.data(), p->d_jobs, K * sizeof(FixJob), cudaMemcpyDeviceToHost, st));
@@ -1032,21 +1108,23 @@ void fill_lists(tfft_plan* p, int scheme, tfft_report* rep, const std::vector<in
         rep->recompute_count = (int64_t)fix_groups.size();
         rep->pass_count += 2 * (int64_t)p->nstages * rep->recompute_count;
     }
-    std::vector<int64_t> unrec = bad_groups;
-    int64_t nc = 0;
+    std::vector<int64_t>& unrec = p->last_unrec;
+    unrec = bad_groups;
+    p->last_corrected.clear();
     for (size_t i = 0; i < fix_groups.size(); ++i) {
         if (fixed_ok[i]) {
+            const int64_t nc = (int64_t)p->last_corrected.size();
             if (nc < rep->corrected_cap) {
                 rep->corrected_group[nc] = fix_groups[i];
                 rep->corrected_signal[nc] = fix_sig[i];
             }
-            ++nc;
+            p->last_corrected.emplace_back(fix_groups[i], fix_sig[i]);
         } else {
             unrec.push_back(fix_groups[i]);
         }
     }
     std::sort(unrec.begin(), unrec.end());
-    rep->n_corrected = nc;
+    rep->n_corrected = (int64_t)p->last_corrected.size();
     rep->n_unrecoverable = (int64_t)unrec.size();
     for (size_t i = 0; i < unrec.size() && (int64_t)i < rep->unrecoverable_cap; ++i) rep->unrecoverable[i] = unrec[i];
 }
@@ -1062,7 +1140,7 @@ int tfft_protect_finish(tfft_plan* p, const void* in, void* out, int64_t batch, 
     if (rc) return rc;
     cudaStream_t st = (cudaStream_t)stream;
     if (!rep) return fail(TFFT_EINVAL, "null report");
-    if (scheme == TFFT_SCHEME_NONE) return TFFT_OK;
+    if (scheme == TFFT_SCHEME_NONE || batch == 0) return TFFT_OK;
     if (!p->ev_done) return fail(TFFT_EINVAL, "tfft_protect_finish without tfft_protect_launch");
     std::vector<std::pair<long long, double>> flags;
     RecheckFn resolve = [&](const std::vector<long long>& sg, std::vector<double>& rr) {
@@ -1162,6 +1240,7 @@ int tfft_run_protected_host(tfft_plan* p, const void* in, void* out, int64_t bat
     Launch L;
     rc = prepare_protected(p, in, out, batch, scheme, delta, etw, values, abs_floor, fault, inverse, rep, L);
     if (rc) return rc;
+    if (batch == 0) return TFFT_OK;
     const bool prot = scheme != TFFT_SCHEME_NONE;
     const size_t sig_bytes = (size_t)p->n * p->esize;
     const size_t grp_bytes = sig_bytes * p->bs;
@@ -1215,18 +1294,14 @@ int tfft_run_protected_host(tfft_plan* p, const void* in, void* out, int64_t bat
     CU(cudaStreamSynchronize(st));
     std::vector<std::pair<long long, double>> flags;
     RecheckFn resolve = [&](const std::vector<long long>& sg, std::vector<double>& rr) {
-        rr.assign(sg.size(), 0.0);
-        char* din = (char*)p->ring;
-        char* dout = din + p->ring_chunk;
-        for (size_t i = 0; i < sg.size(); ++i) {  // rare: stage the signal's input and output rows
-            CU(cudaMemcpyAsync(din, (const char*)in + sg[i] * sig_bytes, sig_bytes, cudaMemcpyHostToDevice, st));
-            CU(cudaMemcpyAsync(dout, (const char*)out + sg[i] * sig_bytes, sig_bytes, cudaMemcpyHostToDevice, st));
-            std::vector<double> r1;
-            int rc2 = recheck_device(p, din, dout, {0}, etw, values, abs_floor, r1, st);
-            if (rc2) return rc2;
-            rr[i] = r1[0];
-        }
-        return (int)TFFT_OK;
+        // rare: stage the signals' input and output rows
+        StageFn stage = [&](int64_t first, int64_t cnt, char* di, char* dq) {
+            CU(cudaMemcpyAsync(di, (const char*)in + first * sig_bytes, cnt * sig_bytes, cudaMemcpyHostToDevice, st));
+            CU(cudaMemcpyAsync(dq, (const char*)out + first * sig_bytes, cnt * sig_bytes, cudaMemcpyHostToDevice,
+                               st));
+            return (int)TFFT_OK;
+        };
+        return recheck_staged(p, sg, rr, etw, values, abs_floor, stage, st);
     };
     rc = read_summary(p, batch, st, rep, flags, delta, resolve);
     if (rc) return rc;
@@ -1395,6 +1470,21 @@ bool read_at(int fd, void* buf, size_t bytes, off_t off) {
     }
     return true;
 }
+// Temp output of an in-place file transform: renamed over `target` by
+// commit(), removed if the call fails before that.
+struct TempOut {
+    std::string path, target;
+    int commit() {
+        if (path.empty()) return TFFT_OK;
+        if (rename(path.c_str(), target.c_str()) != 0) return io_fail("cannot replace", target.c_str());
+        path.clear();
+        return TFFT_OK;
+    }
+    ~TempOut() {
+        if (!path.empty()) unlink(path.c_str());
+    }
+};
+
 bool write_at(int fd, const void* buf, size_t bytes, off_t off) {
     const char* b = (const char*)buf;
     while (bytes) {
@@ -1449,8 +1539,33 @@ int tfft_run_protected_file(tfft_plan* p, const char* in_path, const char* out_p
     Fd fin, fout;
     fin.fd = open(in_path, O_RDONLY);
     if (fin.fd < 0) return io_fail("cannot open", in_path);
-    fout.fd = open(out_path, O_WRONLY | O_CREAT | O_TRUNC, 0644);
-    if (fout.fd < 0) return io_fail("cannot create", out_path);
+    // Output == input (the same file, or a link to it): the reference reads
+    // the whole input before it writes (cli.py:54-67), so the result streams
+    // into a temp file next to the target and is renamed over it at the end;
+    // the input stays intact until then (also on failure: the temp is removed).
+    TempOut tmp;
+    std::string wpath = out_path;
+    {
+        struct stat si, so;
+        if (fstat(fin.fd, &si) == 0 && stat(out_path, &so) == 0 && si.st_dev == so.st_dev && si.st_ino == so.st_ino) {
+            char* real = realpath(out_path, nullptr);
+            if (!real) return io_fail("cannot resolve", out_path);
+            tmp.target = real;
+            free(real);
+            std::string t = tmp.target + ".tfft-XXXXXX";
+            std::vector<char> tmpl(t.begin(), t.end());
+            tmpl.push_back(0);
+            fout.fd = mkstemp(tmpl.data());
+            if (fout.fd < 0) return io_fail("cannot create a temp file for", out_path);
+            tmp.path = tmpl.data();
+            if (fchmod(fout.fd, so.st_mode & 07777) != 0) return io_fail("cannot chmod", tmp.path.c_str());
+            wpath = tmp.path;
+        }
+    }
+    if (tmp.path.empty()) {
+        fout.fd = open(out_path, O_WRONLY | O_CREAT | O_TRUNC, 0644);
+        if (fout.fd < 0) return io_fail("cannot create", out_path);
+    }
     const size_t sig_bytes = (size_t)p->n * p->esize;
     const size_t grp_bytes = sig_bytes * p->bs;
     if (ftruncate(fout.fd, (off_t)(batch * sig_bytes)) != 0) return io_fail("cannot size", out_path);
@@ -1565,29 +1680,26 @@ int tfft_run_protected_file(tfft_plan* p, const char* in_path, const char* out_p
     writer.join();
     if (werr.load()) return fail(werr.load(), werr_msg);
     CU(cudaStreamSynchronize(p->s_d2h));
-    if (!prot) return TFFT_OK;
+    if (!prot) return tmp.commit();
     rc = enqueue_summary(p, st);
     if (rc) return rc;
     std::vector<std::pair<long long, double>> flags;
     RecheckFn resolve = [&](const std::vector<long long>& sg, std::vector<double>& rr) {
-        rr.assign(sg.size(), 0.0);
-        char* din = (char*)p->ring;
-        char* dout = din + p->ring_chunk;
         Fd fo;
-        fo.fd = open(out_path, O_RDONLY);
-        if (fo.fd < 0) return io_fail("cannot reopen", out_path);
-        for (size_t i = 0; i < sg.size(); ++i) {  // rare: re-stage the signal's rows from the files
-            const off_t off = (off_t)(sg[i] * sig_bytes);
-            if (!read_at(fin.fd, hin(0), sig_bytes, off)) return io_fail("cannot read", in_path);
-            if (!read_at(fo.fd, hout(0), sig_bytes, off)) return io_fail("cannot read", out_path);
-            CU(cudaMemcpyAsync(din, hin(0), sig_bytes, cudaMemcpyHostToDevice, st));
-            CU(cudaMemcpyAsync(dout, hout(0), sig_bytes, cudaMemcpyHostToDevice, st));
-            std::vector<double> r1;
-            int rc2 = recheck_device(p, din, dout, {0}, etw, values, abs_floor, r1, st);
-            if (rc2) return rc2;
-            rr[i] = r1[0];
-        }
-        return (int)TFFT_OK;
+        fo.fd = open(wpath.c_str(), O_RDONLY);
+        if (fo.fd < 0) return io_fail("cannot reopen", wpath.c_str());
+        // rare: re-stage the signals' rows from the files
+        StageFn stage = [&](int64_t first, int64_t cnt, char* di, char* dq) {
+            const off_t off = (off_t)(first * sig_bytes);
+            const size_t bytes = (size_t)cnt * sig_bytes;
+            CU(cudaStreamSynchronize(st));  // the pinned slot is reused per run
+            if (!read_at(fin.fd, hin(0), bytes, off)) return io_fail("cannot read", in_path);
+            if (!read_at(fo.fd, hout(0), bytes, off)) return io_fail("cannot read", wpath.c_str());
+            CU(cudaMemcpyAsync(di, hin(0), bytes, cudaMemcpyHostToDevice, st));
+            CU(cudaMemcpyAsync(dq, hout(0), bytes, cudaMemcpyHostToDevice, st));
+            return (int)TFFT_OK;
+        };
+        return recheck_staged(p, sg, rr, etw, values, abs_floor, stage, st);
     };
     rc = read_summary(p, batch, st, rep, flags, delta, resolve);
     if (rc) return rc;
@@ -1598,15 +1710,15 @@ int tfft_run_protected_file(tfft_plan* p, const char* in_path, const char* out_p
     // re-staged from the files, corrected on the device and written back
     char* din = (char*)p->ring;
     char* dout = din + p->ring_chunk;
-    int infd2 = open(out_path, O_RDONLY);
-    if (!fix_groups.empty() && infd2 < 0) return io_fail("cannot reopen", out_path);
+    int infd2 = open(wpath.c_str(), O_RDONLY);
+    if (!fix_groups.empty() && infd2 < 0) return io_fail("cannot reopen", wpath.c_str());
     Fd fo2;
     fo2.fd = infd2;
     for (size_t i = 0; i < fix_groups.size(); ++i) {
         const int64_t g = fix_groups[i];
         const off_t off = (off_t)(g * grp_bytes);
         if (!read_at(fin.fd, hin(0), grp_bytes, off)) return io_fail("cannot read", in_path);
-        if (!read_at(fo2.fd, hout(0), grp_bytes, off)) return io_fail("cannot read", out_path);
+        if (!read_at(fo2.fd, hout(0), grp_bytes, off)) return io_fail("cannot read", wpath.c_str());
         CU(cudaMemcpyAsync(din, hin(0), grp_bytes, cudaMemcpyHostToDevice, st));
         CU(cudaMemcpyAsync(dout, hout(0), grp_bytes, cudaMemcpyHostToDevice, st));
         std::vector<int64_t> g1{0}, s1{fix_sig[i] - g * p->bs};
@@ -1621,7 +1733,7 @@ int tfft_run_protected_file(tfft_plan* p, const char* in_path, const char* out_p
         fixed_ok[i] = ok1[0];
     }
     fill_lists(p, scheme, rep, bad_groups, fix_groups, fix_sig, fixed_ok);
-    return TFFT_OK;
+    return tmp.commit();
 }
 
 }  // extern "C"
@@ -1634,7 +1746,7 @@ int tfft_element_encode(int r, int64_t B, const void* x, void* y, const void* et
     if (!x || !y || !etw_row || !vals_col || !row_in || !xe) return fail(TFFT_EINVAL, "null buffer");
     cudaStream_t st = (cudaStream_t)stream;
     const int grid = (int)std::min<long long>((B + 127) / 128, 1024);
-    element_encode_kernel<<<std::max(grid, 1), 128, 0, st>>>(r, B, (const double2*)x, (const double2*)etw_row,
+    tfft::note_launch(), element_encode_kernel<<<std::max(grid, 1), 128, 0, st>>>(r, B, (const double2*)x, (const double2*)etw_row,
                                                                (const double2*)vals_col, (double2*)y,
                                                                (double2*)row_in, (double2*)xe);
     CU(cudaGetLastError());
@@ -1650,7 +1762,7 @@ int tfft_element_verify(int r, int64_t B, void* y, const void* row_in, const voi
     int* d_res = nullptr;
     CU(cudaMallocAsync((void**)&d_res, 3 * sizeof(int), st));
     CU(cudaMemsetAsync(d_res, 0, 3 * sizeof(int), st));
-    element_verify_kernel<<<1, AUX_THREADS, 0, st>>>(r, B, (double2*)y, (const double2*)row_in, (const double2*)xe,
+    tfft::note_launch(), element_verify_kernel<<<1, AUX_THREADS, 0, st>>>(r, B, (double2*)y, (const double2*)row_in, (const double2*)xe,
                                                      (const double2*)vals_row, (const double2*)vals_col, delta,
                                                      abs_floor, (double*)rel, d_res);
     CU(cudaGetLastError());
@@ -1675,6 +1787,54 @@ int tfft_set_check_level(tfft_plan* p, int level) {
 }  // extern "C"
 
 extern "C" {
+
+int tfft_dft(const void* in, void* out, int64_t batch, int64_t n, int inverse, void* stream) {
+    if (n < 1 || batch < 0) return fail(TFFT_EINVAL, "bad shape");
+    if (n > (int64_t(1) << 14)) return fail(TFFT_EINVAL, "oracle limited to n <= 16384");
+    if (batch == 0) return TFFT_OK;
+    if (!in || !out) return fail(TFFT_EINVAL, "null buffer");
+    cudaStream_t st = (cudaStream_t)stream;
+    // w^m = exp(-+ 2 pi i m / n), m < n, rounded once from long double
+    std::vector<double2> w(n);
+    const long double two_pi = 6.283185307179586476925286766559005768L;
+    for (int64_t m = 0; m < n; ++m) {
+        const long double a = two_pi * (long double)m / (long double)n;
+        w[m] = make_double2((double)cosl(a), (double)((inverse ? 1.0L : -1.0L) * sinl(a)));
+    }
+    double2* dw = nullptr;
+    CU(cudaMallocAsync((void**)&dw, n * sizeof(double2), st));
+    CU(cudaMemcpyAsync(dw, w.data(), n * sizeof(double2), cudaMemcpyHostToDevice, st));
+    for (int64_t b0 = 0; b0 < batch; b0 += 65535) {
+        const int64_t nb = std::min<int64_t>(65535, batch - b0);
+        tfft::note_launch(), dft_direct_kernel<<<dim3((unsigned)((n + 255) / 256), (unsigned)nb), 256, 0, st>>>(
+            (const double2*)in + b0 * n, (double2*)out + b0 * n, n, dw, inverse ? 1.0 / (double)n : 1.0);
+        CU(cudaGetLastError());
+    }
+    CU(cudaFreeAsync(dw, st));
+    CU(cudaStreamSynchronize(st));  // the host table lives on this frame
+    return TFFT_OK;
+}
+
+int tfft_launch_count(int64_t* count) {
+    if (!count) return fail(TFFT_EINVAL, "null argument");
+    *count = tfft::g_launches.load();
+    return TFFT_OK;
+}
+
+int tfft_report_fetch(const tfft_plan* p, tfft_report* rep) {
+    if (!p || !rep) return fail(TFFT_EINVAL, "null argument");
+    rep->n_flagged = (int64_t)p->last_flagged.size();
+    rep->n_corrected = (int64_t)p->last_corrected.size();
+    rep->n_unrecoverable = (int64_t)p->last_unrec.size();
+    for (int64_t i = 0; i < rep->n_flagged && i < rep->flagged_cap; ++i) rep->flagged[i] = p->last_flagged[i];
+    for (int64_t i = 0; i < rep->n_corrected && i < rep->corrected_cap; ++i) {
+        rep->corrected_group[i] = p->last_corrected[i].first;
+        rep->corrected_signal[i] = p->last_corrected[i].second;
+    }
+    for (int64_t i = 0; i < rep->n_unrecoverable && i < rep->unrecoverable_cap; ++i)
+        rep->unrecoverable[i] = p->last_unrec[i];
+    return TFFT_OK;
+}
 
 int tfft_plan_exec_passes(const tfft_plan* p) {
     if (!p) return -1;

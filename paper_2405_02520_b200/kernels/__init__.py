@@ -20,11 +20,38 @@ from .. import _device, _lib
 
 HAVE_EXT = True
 
+# |base - w_L^k| bound for a factor table to count as the DFT's own (the
+# reference builds it with np.exp in fp64 and casts to the plan dtype, or by
+# the renormalised recurrence: <= ~1e-7 / 1e-14 away)
+_BASE_TOL = {8: 1e-5, 16: 1e-12}
+
+
+def _check_base(base, length, itemsize):
+    """The kernels apply the exactly rounded roots w_L^k; a `base` that is not
+    that table (within rounding) would ask for a different transform, so it
+    is rejected instead of silently ignored (_stockham.pyx:32 multiplies by
+    base[q * stride])."""
+    if base is None:
+        return
+    b = base.detach().cpu().numpy() if isinstance(base, torch.Tensor) else np.asarray(base)
+    half = length // 2
+    if b.shape != (half,):
+        raise ValueError("base must hold L/2 factors")
+    if half == 0:
+        return
+    std = np.exp(-2j * np.pi * np.arange(half) / length)
+    with np.errstate(all="ignore"):
+        err = np.abs(b.astype(np.complex128) - std)
+    if not np.all(err <= _BASE_TOL[itemsize]):
+        raise ValueError("base must be the DFT factor table w_L^k = exp(-2 pi i k / L), k < L/2 "
+                         "(this backend computes the DFT; other factor tables are not supported)")
+
 
 def tile_fft(tiles, base=None, inverse: bool = False):
     if isinstance(tiles, torch.Tensor) and tiles.is_cuda:
         if tiles.dtype not in (torch.complex64, torch.complex128):
             raise TypeError(f"unsupported dtype {tiles.dtype}")
+        _check_base(base, tiles.shape[-1], tiles.element_size())
         x = tiles.contiguous()
         out = torch.empty_like(x)
         t, length = x.shape
@@ -36,8 +63,7 @@ def tile_fft(tiles, base=None, inverse: bool = False):
     if arr.dtype not in (np.complex64, np.complex128):
         raise TypeError(f"unsupported dtype {arr.dtype}")
     t, length = arr.shape
-    if base is not None and length > 1 and np.asarray(base).shape[0] != length // 2:
-        raise ValueError("base must hold L/2 factors")
+    _check_base(base, length, arr.dtype.itemsize)
     out = np.empty_like(arr)
     _device.require_cuda()
     _lib.check(_lib.load().tfft_tile_fft(arr.ctypes.data, out.ctypes.data, t, length,

@@ -64,7 +64,7 @@ def transform_file(input_path, output_path, n: int, precision: str = "fp32", sch
     a group is unrecoverable (the report lists it)."""
     from .abft.encoding import EncodingKind, make_encoding
     from .abft.pipeline import DetectionConfig
-    from .abft.protected import RunReport, Scheme, _fault_struct, default_delta
+    from .abft.protected import Scheme, _fault_struct, _report_buffers, default_delta, report_from_native
     from .fault_lab.bits import BitFlipInjector
     from .fft_core import PassCounter, fit_group_size, make_plan
     from .fft_core.plan import native_plan
@@ -88,13 +88,7 @@ def transform_file(input_path, output_path, n: int, precision: str = "fp32", sch
             raise TypeError("transform_file takes a BitFlipInjector (or None)")
         if not injector.fired:
             fault = _fault_struct(injector)
-    cap = max(16, min(batch, 1 << 16))
-    flags = (_lib.Flag * cap)()
-    cg, cs, ur = (ctypes.c_int64 * cap)(), (ctypes.c_int64 * cap)(), (ctypes.c_int64 * cap)()
-    rep = _lib.Report()
-    rep.flagged, rep.flagged_cap = flags, cap
-    rep.corrected_group, rep.corrected_signal, rep.corrected_cap = cg, cs, cap
-    rep.unrecoverable, rep.unrecoverable_cap = ur, cap
+    rep, bufs = _report_buffers(64, 64, 64)
     nb = ctypes.c_int64()
     _lib.check(lib.tfft_run_protected_file(
         h.handle, os.fsencode(str(input_path)), os.fsencode(str(output_path)),
@@ -104,13 +98,6 @@ def transform_file(input_path, output_path, n: int, precision: str = "fp32", sch
         "tfft_run_protected_file")
     if fault is not None and rep.fault_fired:
         injector.fired = True
-    report = RunReport(scheme=scheme.value, delta=cfg.delta, groups=int(rep.groups))
-    report.flagged = [{"group": int(flags[i].group), "signal": int(flags[i].signal),
-                       "discrepancy": float(flags[i].discrepancy)} for i in range(min(rep.n_flagged, cap))]
-    report.corrected = [{"group": int(cg[i]), "signal": int(cs[i])} for i in range(min(rep.n_corrected, cap))]
-    report.unrecoverable = [int(ur[i]) for i in range(min(rep.n_unrecoverable, cap))]
-    report.recompute_count = int(rep.recompute_count)
-    report.pass_count = int(rep.pass_count)
-    report.max_rel_discrepancy = float(rep.max_rel_discrepancy)
+    report = report_from_native(lib, h, rep, bufs, scheme, cfg.delta)
     counter = PassCounter(reads=report.pass_count // 2, writes=report.pass_count // 2)
     return report, counter, int(nb.value)

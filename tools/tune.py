@@ -6,6 +6,9 @@ fp64 numpy FFT on a small batch, then times it on a 1 GiB batch with ABFT on
 gpurun_out/tune_single.json. The winners go into codegen.SINGLE_CHOICE.
 
     python tools/tune.py [--sizes 3-13] [--prec fp32,fp64] [--reps 5]
+
+Needs the tuning build (every candidate compiled):
+    TFFT_TUNE=1 python -m paper_2405_02520_b200.build
 """
 
 from __future__ import annotations

@@ -6,6 +6,9 @@ L, stage kind) not tuned yet, times the whole protected transform (ABFT on,
 stages at their current best. Correctness of every variant is checked against
 numpy on a small batch. Prints PASS_CHOICE for codegen.py and writes
 gpurun_out/tune_pass.json.
+
+Needs the tuning build (every candidate compiled):
+    TFFT_TUNE=1 python -m paper_2405_02520_b200.build
 """
 
 from __future__ import annotations
