@@ -33,20 +33,19 @@ def _cases():
     return out
 
 
-@pytest.mark.parametrize("name,kw", _cases(), ids=[c[0] for c in _cases()])
-def test_campaign_matches_reference(name, kw):
-    from paper_2405_02520_b200.fault_lab import (RECORD_COLUMNS, ROC_COLUMNS, CampaignConfig,
-                                                 records_csv, roc_csv, run_campaign)
-    kw = dict(kw)
-    if "bits" in kw:
-        kw["bits"] = tuple(kw["bits"])
-    res = run_campaign(CampaignConfig(**kw))
+def check_against_reference(res, kw, rec_path, roc_path, name):
+    """Record-by-record parity of a device campaign with the reference's CSVs:
+    identical runs and faults; discrepancies within 5 % wherever they are
+    above the clean rounding noise; decisions equal wherever the reference's
+    discrepancy is clear of the thresholds (x3); ROC rates within the share of
+    runs inside that band. Returns the per-run comparison counts."""
+    from paper_2405_02520_b200.fault_lab import RECORD_COLUMNS, ROC_COLUMNS, records_csv, roc_csv
     rec_text = records_csv(res)
     roc_text = roc_csv(res)
     assert rec_text.splitlines()[0] == ",".join(RECORD_COLUMNS)
     assert roc_text.splitlines()[0] == ",".join(ROC_COLUMNS)
     mine = list(csv.DictReader(io.StringIO(rec_text)))
-    ref = _read(os.path.join(GOLD, f"campaign_{name}_records.csv"))
+    ref = _read(rec_path)
     assert len(mine) == len(ref) == kw["runs"]
     fp32 = kw["precision"] == "fp32"
     op_delta = 1e-4 if fp32 else 1e-9
@@ -54,6 +53,7 @@ def test_campaign_matches_reference(name, kw):
     clean_ref = [float(r["discrepancy"]) for r in ref if r["injected"] == "0"]
     ref_dd = 10.0 * float(np.quantile(clean_ref, 0.999))
     assert res.default_delta == pytest.approx(ref_dd, rel=3.0)  # rounding-noise calibrated
+    stats = dict(runs=len(ref), compared_disc=0, compared_detect=0, compared_corrected=0, band=0)
     for m, r in zip(mine, ref):
         for k in ("run_id", "injected", "signal_idx", "element_idx", "bit"):
             assert m[k] == r[k], (name, r["run_id"], k)
@@ -65,15 +65,20 @@ def test_campaign_matches_reference(name, kw):
             assert math.isinf(dm), (name, r["run_id"])
         elif dr > 10 * noise:
             assert dm == pytest.approx(dr, rel=5e-2), (name, r["run_id"])
+            stats["compared_disc"] += 1
         clear = lambda t: not (t / 3 < dr < 3 * t)  # noqa: E731
         if clear(ref_dd) and clear(res.default_delta):
             assert m["detected_at_default_delta"] == r["detected_at_default_delta"], (name, r["run_id"])
+            stats["compared_detect"] += 1
+        else:
+            stats["band"] += 1
         if clear(op_delta) and (dr > 3 * op_delta or dr < noise):
             assert m["corrected"] == r["corrected"], (name, r["run_id"])
+            stats["compared_corrected"] += 1
     # ROC: every rate within the share of reference runs whose discrepancy is
     # inside a factor 3 of that threshold
     roc_m = list(csv.DictReader(io.StringIO(roc_text)))
-    roc_r = _read(os.path.join(GOLD, f"campaign_{name}_roc.csv"))
+    roc_r = _read(roc_path)
     disc_r = np.array([float(r["discrepancy"]) for r in ref])
     assert [row["delta"] for row in roc_m] == [row["delta"] for row in roc_r]
     n_inj = sum(r["injected"] == "1" for r in ref)
@@ -84,6 +89,46 @@ def test_campaign_matches_reference(name, kw):
         for k in ROC_COLUMNS[1:]:
             slack = near / max(min(n_inj, n_clean), 1) + 1e-12
             assert abs(float(a[k]) - float(b[k])) <= slack, (name, d, k)
+    return stats
+
+
+@pytest.mark.parametrize("name,kw", _cases(), ids=[c[0] for c in _cases()])
+def test_campaign_matches_reference(name, kw):
+    from paper_2405_02520_b200.fault_lab import CampaignConfig, run_campaign
+    kw = dict(kw)
+    if "bits" in kw:
+        kw["bits"] = tuple(kw["bits"])
+    res = run_campaign(CampaignConfig(**kw))
+    check_against_reference(res, kw, os.path.join(GOLD, f"campaign_{name}_records.csv"),
+                            os.path.join(GOLD, f"campaign_{name}_roc.csv"), name)
+
+
+C4 = json.load(open(os.path.join(GOLD, "c4_summary.json")))
+
+
+@pytest.mark.parametrize("name", ["fp32", "fp64", "fp32_exp", "fp64_exp"])
+def test_c4_campaign_matches_reference(name):
+    """SURVEY §8(d) C4 at its stated size: run_campaign(CampaignConfig(
+    runs=2000, inject_fraction=0.5, n=2**16, batch=16, precision=p, seed=1))
+    (+ the exponent-class bit pools), record by record against the REAL
+    reference's CSVs (tests/golden/make_golden_c4.py). The detected /
+    corrected counts equal the reference's up to the runs whose discrepancy
+    lies inside x3 of the calibrated threshold."""
+    from paper_2405_02520_b200.fault_lab import CampaignConfig, run_campaign
+    kw = dict(C4["config"], **C4["variants"][name])
+    if "bits" in kw:
+        kw["bits"] = tuple(kw["bits"])
+    res = run_campaign(CampaignConfig(**kw))
+    stats = check_against_reference(res, kw, os.path.join(GOLD, f"c4_{name}_records.csv"),
+                                    os.path.join(GOLD, f"c4_{name}_roc.csv"), f"c4_{name}")
+    ref = C4[name]
+    assert res.injected_count == ref["injected"] == 1000
+    assert abs(res.detected_count - ref["detected"]) <= stats["band"]
+    assert abs(res.corrected_count - ref["corrected"]) <= stats["band"]
+    assert res.recompute_count == ref["recompute"] == 0
+    if name == "fp64_exp":  # every fp64 exponent-class flip: detected and corrected (as the reference)
+        assert res.detected_count == res.corrected_count == 1000
+    assert stats["compared_detect"] >= 1900 and stats["compared_corrected"] >= 900, stats
 
 
 def test_campaign_exponent_faults_all_detected_and_corrected():
