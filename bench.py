@@ -1,14 +1,25 @@
-"""Benchmark: BASELINE.json configs[1] — FP32 single-kernel FFT sweep
+"""Benchmark: BASELINE.json configs[1] (C2) — the FP32 single-kernel FFT sweep
 N = 2^3 .. 2^13, a 1 GiB batch per size per GPU, two-sided ABFT on
-(two_sided_group), plus ABFT-off and cuFFT (torch.fft) comparisons.
+(two_sided_group) — plus the FP64 multi-pass leg C3 (N = 2^20 .. 2^25, 2 GiB
+per GPU), ABFT-off and cuFFT (torch.fft) comparisons, and the reference's CPU
+path timed beside it.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--strong] [--skip-cpu] [--skip-c3]
 
-One step = one protected pass of the hot path over every size of the sweep
-(11 fused launches, 11 GiB in + 11 GiB out per GPU). Multi-GPU: one process
-per GPU (torchrun), each rank owns its own 1 GiB batches (batch sharding, weak
-scaling); the only collective is an NCCL all-reduce of the fault counters.
-Rank 0 prints one JSON line.
+One step = one protected pass of the hot path over every size of the C2
+sweep (11 fused launches, 11 GiB in + 11 GiB out per GPU; every size writes
+its own output buffer, so flagged groups are corrected on intact data), then
+one NCCL all-reduce of the step's fault counters when N > 1.
+
+Multi-GPU: one process per GPU. Under torchrun the ranks come from the
+environment; `--gpus N` without torchrun spawns the N ranks itself
+(torch.multiprocessing, NCCL). Weak scaling (default): every rank owns its
+own 1 GiB batch per size, i.e. its group-aligned slice of an N GiB global
+batch. `--strong`: the global batch per size stays 1 GiB and each rank owns
+1/N of it. The e2e leg drives the public sharded API
+(`sharding.run_protected_sharded`) with host buffers. Rank 0 prints one JSON
+line; times are the max over ranks.
 """
 
 from __future__ import annotations
@@ -19,7 +30,6 @@ import json
 import math
 import os
 import statistics
-import subprocess
 import sys
 import threading
 import time
@@ -30,8 +40,10 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "batched FFT GFLOP/s & HBM GB/s (FP32/FP64, ABFT on) vs roofline; ABFT overhead %"
-SIZES = list(range(3, 14))            # log2 N
-BATCH_BYTES = 1 << 30                 # per size per GPU (complex64 input)
+SIZES = list(range(3, 14))            # C2: log2 N
+C3_SIZES = list(range(20, 26))        # C3: log2 N (fp64, multi-pass)
+BATCH_BYTES = 1 << 30                 # C2: per size per GPU (complex64 input)
+C3_BYTES = 2 << 30                    # C3: per size per GPU (complex128 input)
 WORKLOAD = ("C2: FP32 single-kernel FFT sweep N=2^3..2^13, 1 GiB complex64 batch per size "
             "per GPU, two-sided ABFT (two_sided_group) on")
 
@@ -44,9 +56,9 @@ def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             d = json.load(f)
-        return float(d["hbm_gbs"]), "measured"
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy burst)"
     except Exception:
-        return 6650.0, "fallback"
+        return 6650.0, "fallback (B200_PROFILING.md)"
 
 
 # ------------------------------------------------------------------ clocks
@@ -120,7 +132,8 @@ class ClockSampler:
 
 # -------------------------------------------------------------- CPU baseline
 def _cpu_shard(args):
-    """One worker: the oracle (reference restatement) on a shard of groups."""
+    """One worker: the oracle (reference restatement with the reference's own
+    compiled Cython butterfly) on a shard of checksum groups."""
     logn, nsig, seed, kernel = args
     sys.path.insert(0, ROOT)
     from oracle import port as P
@@ -135,201 +148,281 @@ def _cpu_shard(args):
     return time.perf_counter() - t0
 
 
-def cpu_reference(sample_elems=1 << 22, cores=None):
-    """Time the reference CPU path (oracle port; the reference's own compiled
-    Cython butterfly when oracle/_ref is built) over a bounded sample of the
-    sweep: `sample_elems` complex64 samples per size, sharded by checksum
-    group over all host cores. Each shard times only its run_protected call;
-    the parallel time is the sum of shard times / cores (shards are
-    independent, so this is the ideal all-core throughput of the reference).
-    Returns (GFLOP/s, cores, sample text, kind)."""
+def _cpu_jobs(sample_elems, shards_per_size):
+    jobs, total = [], 0.0
+    for logn in SIZES:
+        n = 1 << logn
+        nsig = max(16, sample_elems // n)
+        per = max(16, (nsig // shards_per_size) // 16 * 16)
+        k = max(1, nsig // per)
+        jobs += [(logn, per, s, None) for s in range(k)]
+        total += flops(n, per * k)
+    return jobs, total
+
+
+def cpu_reference(cores=None, single_elems=1 << 18, multi_elems=1 << 22):
+    """The reference's CPU path (oracle port; butterflies by the reference's
+    own compiled `_stockham` when oracle/_ref is built) over bounded samples
+    of the C2 sweep, measured two ways:
+      * 1 core: one process, `single_elems` complex64 samples per size, the
+        summed run_protected time (the reference as shipped is single-threaded);
+      * all cores: `multi_elems` samples per size sharded by checksum group over
+        a pool of `cores` processes, timed as the WALL time of the pool map
+        (workers warmed first; the wall includes each shard's seeded input draw).
+    Returns a dict with both GFLOP/s figures."""
     import multiprocessing as mp
     from oracle import port as P
     kernel = "ref" if P.have_ref_kernel() else "c"
     cores = cores or os.cpu_count() or 1
-    jobs = []
-    total_flops = 0.0
-    for logn in SIZES:
-        n = 1 << logn
-        nsig = max(16, sample_elems // n)
-        per = max(16, (nsig // cores) // 16 * 16)
-        shards = max(1, nsig // per)
-        for s in range(shards):
-            jobs.append((logn, per, s, kernel))
-        total_flops += flops(n, per * shards)
+    jobs1, fl1 = _cpu_jobs(single_elems, 1)
+    jobs1 = [(a, b, c, kernel) for a, b, c, _ in jobs1]
+    t1 = sum(_cpu_shard(j) for j in jobs1)
+    jobsn, fln = _cpu_jobs(multi_elems, cores)
+    jobsn = [(a, b, c, kernel) for a, b, c, _ in jobsn]
     ctx = mp.get_context("fork")
     with ctx.Pool(cores) as pool:
-        times = pool.map(_cpu_shard, jobs, chunksize=1)
-    par = sum(times) / cores
-    sample = (f"{sample_elems} complex64 samples per size, N=2^3..2^13 ({len(jobs)} shards), "
-              f"run_protected two_sided_group (Wang encoding precomputed), sharded by checksum "
-              f"group over {cores} processes, time = sum(shard times)/cores; butterfly kernel: "
-              f"{'reference _stockham compiled from /root/reference (oracle/_ref)' if kernel == 'ref' else 'C restatement (oracle/stockham.c)'}")
-    return total_flops / par / 1e9, cores, sample, "port"
+        pool.map(_cpu_shard, [(3, 16, 0, kernel)] * cores)  # warm the workers (imports, kernel load)
+        w0 = time.perf_counter()
+        shard_t = pool.map(_cpu_shard, jobsn, chunksize=1)
+        wall = time.perf_counter() - w0
+    butterfly = ("reference _stockham compiled from /root/reference (oracle/_ref)" if kernel == "ref"
+                 else "C restatement (oracle/stockham.c)")
+    return {
+        "one_core_gflops": fl1 / t1 / 1e9, "one_core_s": t1,
+        "all_core_gflops": fln / wall / 1e9, "all_core_wall_s": wall,
+        "all_core_busy_s": sum(shard_t), "cores": cores, "kind": "port",
+        "sample": (f"C2 sweep N=2^3..2^13, run_protected two_sided_group (Wang encoding "
+                   f"precomputed); 1 core (input draw outside the clock): {single_elems} complex64 "
+                   f"samples per size in one process; all cores: {multi_elems} samples per size in "
+                   f"{len(jobsn)} group-aligned shards over {cores} processes, pool wall time incl. each shard's input draw; "
+                   f"butterfly: {butterfly}"),
+    }
 
 
 # ------------------------------------------------------------------- ours
+class Report:
+    """ctypes report buffers for the launch / finish C ABI."""
+
+    def __init__(self, lib_mod, cap=64):
+        self.rep = lib_mod.Report()
+        self.keep = ((lib_mod.Flag * cap)(), (ctypes.c_int64 * cap)(), (ctypes.c_int64 * cap)(),
+                     (ctypes.c_int64 * cap)())
+        flags, cg, cs, ur = self.keep
+        self.rep.flagged, self.rep.flagged_cap = flags, cap
+        self.rep.corrected_group, self.rep.corrected_signal, self.rep.corrected_cap = cg, cs, cap
+        self.rep.unrecoverable, self.rep.unrecoverable_cap = ur, cap
+
+
+def _cases(prec, sizes, per_rank_bytes, device, dev_index):
+    import torch
+
+    from paper_2405_02520_b200 import _lib, make_plan
+    from paper_2405_02520_b200.abft import make_encoding
+    from paper_2405_02520_b200.fft_core import fit_group_size
+    from paper_2405_02520_b200.fft_core.plan import native_plan
+    esz = 8 if prec == "fp32" else 16
+    td = torch.complex64 if prec == "fp32" else torch.complex128
+    out = []
+    for logn in sizes:
+        n = 1 << logn
+        b = per_rank_bytes // (esz * n)
+        plan = fit_group_size(make_plan(n, prec, batch=b), b)
+        enc = make_encoding("wang", n)
+        h = native_plan(plan, dev_index)
+        out.append(dict(logn=logn, n=n, b=b, plan=plan, h=h, row=enc.device_row(td, False),
+                        y=torch.empty((b, n), dtype=td, device=device), esz=esz,
+                        passes=_lib.load().tfft_plan_exec_passes(h.handle), rep=Report(_lib)))
+    return out
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
 
-    from paper_2405_02520_b200 import _lib, build_twiddles, make_plan, run_protected
-    from paper_2405_02520_b200.abft import DetectionConfig, Scheme, make_encoding
-    from paper_2405_02520_b200.fft_core import fit_group_size
-    from paper_2405_02520_b200.fft_core.plan import native_plan
+    from paper_2405_02520_b200 import _lib, build_twiddles
+    from paper_2405_02520_b200.abft import DetectionConfig, Scheme
+    from paper_2405_02520_b200.sharding import run_protected_sharded
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     lib = _lib.load()
     stream = torch.cuda.current_stream()
     sp = stream.cuda_stream
-    total_elems = BATCH_BYTES // 8
-    g = torch.Generator(device=dev).manual_seed(1234 + rank)
-    x = torch.randn(total_elems, dtype=torch.complex64, device=dev, generator=g)
-    y = torch.empty_like(x)
+    share = world if args.strong else 1
+    c2_bytes = BATCH_BYTES // share
+    x = torch.randn(c2_bytes // 8, dtype=torch.complex64, device=dev,
+                    generator=torch.Generator(device=dev).manual_seed(1234 + rank))
+    cases = _cases("fp32", SIZES, c2_bytes, dev, local_rank)
 
-    cases = []
-    for logn in SIZES:
-        n = 1 << logn
-        b = total_elems // n
-        plan = fit_group_size(make_plan(n, "fp32", batch=b), b)
-        enc = make_encoding("wang", n)
-        row = enc.device_row(torch.complex64, False)
-        h = native_plan(plan, local_rank)
-        rep = _lib.Report()
-        cap = 64
-        flags = (_lib.Flag * cap)()
-        i64 = (ctypes.c_int64 * cap)
-        cg, cs, ur = i64(), i64(), i64()
-        rep.flagged, rep.flagged_cap = flags, cap
-        rep.corrected_group, rep.corrected_signal, rep.corrected_cap = cg, cs, cap
-        rep.unrecoverable, rep.unrecoverable_cap = ur, cap
-        cases.append(dict(logn=logn, n=n, b=b, plan=plan, h=h, row=row, rep=rep,
-                          keep=(flags, cg, cs, ur)))
-
-    def launch(c, scheme):
+    def launch(c, xx, scheme, delta):
         code = _lib.SCHEME_CODE[scheme]
-        _lib.check(lib.tfft_protect_launch(c["h"].handle, x.data_ptr(), y.data_ptr(), c["b"], code,
-                                           1e-4, 0.0, c["row"].data_ptr(), None, None, 0,
-                                           ctypes.byref(c["rep"]), sp), "launch")
+        _lib.check(lib.tfft_protect_launch(c["h"].handle, xx.data_ptr(), c["y"].data_ptr(), c["b"], code,
+                                           delta, 0.0, c["row"].data_ptr(), None, None, 0,
+                                           ctypes.byref(c["rep"].rep), sp), "launch")
 
-    def finish(c, scheme):
+    def finish(c, xx, scheme, delta):
         code = _lib.SCHEME_CODE[scheme]
-        _lib.check(lib.tfft_protect_finish(c["h"].handle, x.data_ptr(), y.data_ptr(), c["b"], code,
-                                           1e-4, 0.0, c["row"].data_ptr(), None, 0,
-                                           ctypes.byref(c["rep"]), sp), "finish")
+        _lib.check(lib.tfft_protect_finish(c["h"].handle, xx.data_ptr(), c["y"].data_ptr(), c["b"], code,
+                                           delta, 0.0, c["row"].data_ptr(), None, 0,
+                                           ctypes.byref(c["rep"].rep), sp), "finish")
 
-    def step(scheme, events=None):
-        for i, c in enumerate(cases):
+    def step(cs, xx, scheme, delta, events=None):
+        """One protected pass over every size: all launches queue first, then
+        the per-size detection summaries are read (and rare flags handled)."""
+        for i, c in enumerate(cs):
             if events is not None:
                 events[i][0].record(stream)
-            launch(c, scheme)
+            launch(c, xx, scheme, delta)
             if events is not None:
                 events[i][1].record(stream)
-        for c in cases:
-            finish(c, scheme)
+        cnt = np.zeros(4, dtype=np.int64)
+        mx = 0.0
+        if scheme != "none":
+            for c in cs:
+                finish(c, xx, scheme, delta)
+                r = c["rep"].rep
+                cnt += np.array([r.n_flagged, r.n_corrected, r.n_unrecoverable, r.recompute_count])
+                mx = max(mx, r.max_rel_discrepancy)
+        return cnt, mx
 
     def barrier():
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
 
-    for _ in range(args.warmup):
-        step("two_sided_group")
-    counters = np.zeros(4, dtype=np.int64)
-    max_rel = 0.0
-    per_n = [[] for _ in cases]
-    clocks = ClockSampler(local_rank)
-    barrier()
-    clocks.start()
-    t_start = torch.cuda.Event(enable_timing=True)
-    t_end = torch.cuda.Event(enable_timing=True)
-    evs = [[[torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)]
-            for _ in cases] for _ in range(args.steps)]
-    t_start.record(stream)
-    for s in range(args.steps):
-        step("two_sided_group", evs[s])
-        for c in cases:
-            r = c["rep"]
-            counters += np.array([r.n_flagged, r.n_corrected, r.n_unrecoverable, r.recompute_count])
-            max_rel = max(max_rel, r.max_rel_discrepancy)
-    t_end.record(stream)
-    barrier()
-    clk = clocks.stop()
-    ms_total = t_start.elapsed_time(t_end)
-    for s in range(args.steps):
-        for i in range(len(cases)):
-            per_n[i].append(evs[s][i][0].elapsed_time(evs[s][i][1]))
-    ms_step_local = ms_total / args.steps
-
-    # ---- ABFT off and cuFFT on the same buffers (outside the timed region)
-    off_n, cufft_n = [[] for _ in cases], [[] for _ in cases]
-    for _ in range(2):
-        step("none")
-    for s in range(args.steps):
-        ev = [[torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)]
-              for _ in cases]
-        step("none", ev)
-        torch.cuda.synchronize()
-        for i in range(len(cases)):
-            off_n[i].append(ev[i][0].elapsed_time(ev[i][1]))
-    for i, c in enumerate(cases):
-        xv = x.view(c["b"], c["n"])
-        yv = y.view(c["b"], c["n"])
-        torch.fft.fft(xv, out=yv)
-        for _ in range(args.steps):
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            torch.fft.fft(xv, out=yv)
-            e1.record(stream)
-            torch.cuda.synchronize()
-            cufft_n[i].append(e0.elapsed_time(e1))
-
-    # ---- collectives: max step time over ranks, NCCL-reduced fault counters
-    ms_step = ms_step_local
-    if world > 1:
-        t = torch.tensor([ms_step_local], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_step = float(t.item())
-        ct = torch.tensor(counters, device=dev)
+    def reduce_counts(cnt, mx):
+        """The protected path's one collective: sum of the fault counters
+        (and max of the max discrepancy) over the ranks."""
+        if world == 1:
+            return cnt, mx
+        t = torch.tensor(list(cnt) + [0], dtype=torch.float64, device=dev)
+        t[-1] = mx
+        ct = t[:-1].clone()
         dist.all_reduce(ct, op=dist.ReduceOp.SUM)
-        counters = ct.cpu().numpy()
-        mr = torch.tensor([max_rel], device=dev, dtype=torch.float64)
-        dist.all_reduce(mr, op=dist.ReduceOp.MAX)
-        max_rel = float(mr.item())
+        m = t[-1:].clone()
+        dist.all_reduce(m, op=dist.ReduceOp.MAX)
+        return ct.cpu().numpy().astype(np.int64), float(m.item())
 
-    # ---- e2e: public API, host (pinned) buffers, H2D + D2H inside the timed region
-    e2e = None
-    if rank == 0 or world > 1:
-        xh = x.cpu().pin_memory()
-        e2e_steps = max(1, min(args.steps, 3))
-        cfg = DetectionConfig(delta=1e-4)
-        tws = [build_twiddles(c["plan"]) for c in cases]
-        out = None
-        for _ in range(2):  # warm exactly like the timed loop (encodings, both pinned output blocks)
-            for c, tw in zip(cases, tws):
-                out, rep, _ = run_protected(c["plan"], tw, xh.view(c["b"], c["n"]),
-                                            Scheme.TWO_SIDED_GROUP, cfg)
+    def timed(cs, xx, scheme, delta, steps):
+        counters = np.zeros(4, dtype=np.int64)
+        max_rel = 0.0
+        per = [[] for _ in cs]
+        clocks = ClockSampler(local_rank)
         barrier()
-        t0 = time.perf_counter()
-        for _ in range(e2e_steps):
-            for c, tw in zip(cases, tws):
-                out, rep, _ = run_protected(c["plan"], tw, xh.view(c["b"], c["n"]),
-                                            Scheme.TWO_SIDED_GROUP, cfg)
-        torch.cuda.synchronize()
-        e2e_ms = (time.perf_counter() - t0) * 1000 / e2e_steps
-        if world > 1:
-            t = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e_ms = float(t.item())
-        step_flops_all = world * sum(flops(c["n"], c["b"]) for c in cases)
-        e2e = {"value": step_flops_all / (e2e_ms / 1000) / 1e9, "unit": "GFLOP/s",
-               "ms_per_step": e2e_ms,
-               "h2d_bytes_per_step": int(sum(c["b"] * c["n"] * 8 for c in cases)),
-               "d2h_bytes_per_step": int(sum(c["b"] * c["n"] * 8 for c in cases)),
-               "api": ("paper_2405_02520_b200.run_protected(pinned host batch -> numpy) -> C-ABI "
-                       "tfft_run_protected_host: H2D / fused transform / D2H streamed in 32 MiB "
-                       "group-aligned chunks on three streams")}
+        l0 = _lib.launch_count()
+        clocks.start()
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        evs = [[[torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)]
+                for _ in cs] for _ in range(steps)]
+        t0.record(stream)
+        for s in range(steps):
+            cnt, mx = step(cs, xx, scheme, delta, evs[s])
+            cnt, mx = reduce_counts(cnt, mx)
+            counters += cnt
+            max_rel = max(max_rel, mx)
+        t1.record(stream)
+        barrier()
+        clk = clocks.stop()
+        launches = _lib.launch_count() - l0
+        for s in range(steps):
+            for i in range(len(cs)):
+                per[i].append(evs[s][i][0].elapsed_time(evs[s][i][1]))
+        ms_local = t0.elapsed_time(t1) / steps
+        return ms_local, per, counters, max_rel, clk, launches
+
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def off_and_cufft(cs, xx, reps):
+        off, cuf = [[] for _ in cs], [[] for _ in cs]
+        step(cs, xx, "none", 1.0)
+        for _ in range(reps):
+            ev = [[torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)] for _ in cs]
+            step(cs, xx, "none", 1.0, ev)
+            torch.cuda.synchronize()
+            for i in range(len(cs)):
+                off[i].append(ev[i][0].elapsed_time(ev[i][1]))
+        for i, c in enumerate(cs):
+            xv = xx[:c["b"] * c["n"]].view(c["b"], c["n"])
+            torch.fft.fft(xv, out=c["y"])
+            for _ in range(reps):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                torch.fft.fft(xv, out=c["y"])
+                e1.record(stream)
+                torch.cuda.synchronize()
+                cuf[i].append(e0.elapsed_time(e1))
+        return off, cuf
+
+    # ---------------------------------------------------------------- C2
+    for _ in range(args.warmup):
+        step(cases, x, "two_sided_group", 1e-4)
+    ms_local, per_n, counters, max_rel, clk, launches = timed(cases, x, "two_sided_group", 1e-4, args.steps)
+    ms_step = max_over_ranks(ms_local)
+    off_n, cufft_n = off_and_cufft(cases, x, max(3, min(args.steps, 10)))
+
+    # ---------------------------------------------------------------- e2e
+    # the public API with host (pinned) buffers: H2D and D2H inside the timed
+    # region; at N > 1 through sharding.run_protected_sharded (global batch =
+    # the ranks' slices, start = rank's offset), counters reduced over NCCL
+    xh = x.cpu().pin_memory()
+    cfg = DetectionConfig(delta=1e-4)
+    tws = [build_twiddles(c["plan"]) for c in cases]
+
+    def api_step():
+        for c, tw in zip(cases, tws):
+            xv = xh[:c["b"] * c["n"]].view(c["b"], c["n"])
+            out, rep, _ = run_protected_sharded(c["plan"], tw, xv, rank * c["b"], Scheme.TWO_SIDED_GROUP,
+                                                cfg)
+        return out
+
+    for _ in range(2):  # warm exactly like the timed loop (encodings, pinned output blocks)
+        api_step()
+    e2e_steps = max(1, min(args.steps, 3))
+    barrier()
+    w0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        api_step()
+    torch.cuda.synchronize()
+    e2e_ms = max_over_ranks((time.perf_counter() - w0) * 1000 / e2e_steps)
+    step_flops_all = world * sum(flops(c["n"], c["b"]) for c in cases)
+    e2e = {"value": round(step_flops_all / (e2e_ms / 1000) / 1e9, 1), "unit": "GFLOP/s",
+           "ms_per_step": round(e2e_ms, 3),
+           "h2d_bytes_per_step": int(sum(c["b"] * c["n"] * 8 for c in cases)),
+           "d2h_bytes_per_step": int(sum(c["b"] * c["n"] * 8 for c in cases)),
+           "api": ("paper_2405_02520_b200.sharding.run_protected_sharded(pinned host slice -> numpy) "
+                   "-> run_protected -> C-ABI tfft_run_protected_host (H2D / fused transform / D2H "
+                   "streamed in 32 MiB group-aligned chunks on three streams) + NCCL counter reduce"
+                   if world > 1 else
+                   "paper_2405_02520_b200.run_protected(pinned host batch -> numpy) via "
+                   "sharding.run_protected_sharded (world 1) -> C-ABI tfft_run_protected_host: H2D / "
+                   "fused transform / D2H streamed in 32 MiB group-aligned chunks on three streams")}
+    del xh
+
+    # ---------------------------------------------------------------- C3
+    c3 = None
+    if not args.skip_c3:
+        for c in cases:
+            del c["y"]
+        del x
+        torch.cuda.empty_cache()
+        c3_bytes = C3_BYTES // share
+        x3 = torch.randn(c3_bytes // 16, dtype=torch.complex128, device=dev,
+                         generator=torch.Generator(device=dev).manual_seed(4321 + rank))
+        cases3 = _cases("fp64", C3_SIZES, c3_bytes, dev, local_rank)
+        for _ in range(max(2, args.warmup)):
+            step(cases3, x3, "two_sided_group", 1e-9)
+        steps3 = max(3, min(args.steps, 10))
+        ms3, per3, cnt3, mx3, clk3, launches3 = timed(cases3, x3, "two_sided_group", 1e-9, steps3)
+        ms3 = max_over_ranks(ms3)
+        off3, cuf3 = off_and_cufft(cases3, x3, 3)
+        c3 = dict(cases=cases3, per=per3, off=off3, cuf=cuf3, ms=ms3, cnt=cnt3, mx=mx3, clk=clk3,
+                  launches=launches3, steps=steps3)
+        del x3
 
     if rank != 0:
         return
@@ -358,20 +451,63 @@ def run_ours(args, rank, world, local_rank):
     # list (tools/launch_summary.py), averaged over the sweep's launches like
     # `achieved` (algorithmic: 2 GiB per launch)
     traffic = None
-    tpath = os.path.join(ROOT, "profiles", "traffic_r01.json")
-    if os.path.exists(tpath):
-        try:
-            by_n = json.load(open(tpath))["dram_bytes_per_launch_by_n"]
-            vals = [by_n[str(c["n"])] for c in cases if str(c["n"]) in by_n]
-            if len(vals) == len(cases):
-                traffic = round(sum(vals) / len(vals))
-        except Exception:
-            traffic = None
+    for tname in ("traffic_r02.json", "traffic_r01.json"):
+        tpath = os.path.join(ROOT, "profiles", tname)
+        if traffic is None and os.path.exists(tpath):
+            try:
+                by_n = json.load(open(tpath))["dram_bytes_per_launch_by_n"]
+                vals = [by_n[str(c["n"])] for c in cases if str(c["n"]) in by_n]
+                if len(vals) == len(cases):
+                    traffic = round(sum(vals) / len(vals))
+            except Exception:
+                traffic = None
     cpu = None
     if world == 1 and not args.skip_cpu:
-        v, cores, sample, kind = cpu_reference()
-        cpu = {"value": round(v, 4), "unit": "GFLOP/s", "cores": cores, "kind": kind,
-               "sample": sample}
+        cr = cpu_reference()
+        cpu = {"value": round(cr["all_core_gflops"], 4), "unit": "GFLOP/s", "cores": cr["cores"],
+               "kind": cr["kind"], "sample": cr["sample"],
+               "one_core": {"value": round(cr["one_core_gflops"], 4), "unit": "GFLOP/s", "cores": 1,
+                            "seconds": round(cr["one_core_s"], 2)},
+               "all_core_wall_s": round(cr["all_core_wall_s"], 2),
+               "all_core_busy_s": round(cr["all_core_busy_s"], 2)}
+    c3_out = None
+    if c3 is not None:
+        rows = []
+        t_on = t_off = t_cf = by_exec = by_min = 0.0
+        for i, c in enumerate(c3["cases"]):
+            on = statistics.median(c3["per"][i])
+            off = statistics.median(c3["off"][i])
+            cf = statistics.median(c3["cuf"][i])
+            per_pass = 2.0 * c["b"] * c["n"] * 16
+            t_on += on
+            t_off += off
+            t_cf += cf
+            by_exec += c["passes"] * per_pass
+            by_min += 2 * per_pass
+            rows.append({"n": c["n"], "batch": c["b"], "passes": c["passes"], "ms_abft_on": round(on, 4),
+                         "ms_abft_off": round(off, 4), "ms_cufft": round(cf, 4),
+                         "gflops_abft_on": round(flops(c["n"], c["b"]) / on / 1e6, 1),
+                         "hbm_gbs_per_executed_pass": round(c["passes"] * per_pass / on / 1e6, 1),
+                         "frac_per_executed_pass": round(c["passes"] * per_pass / on / 1e6 / hbm, 4),
+                         "frac_vs_2pass_minimum": round(2 * per_pass / on / 1e6 / hbm, 4),
+                         "abft_overhead_pct": round(100 * (on / off - 1), 2),
+                         "vs_cufft": round(cf / on, 4)})
+        c3_out = {
+            "workload": ("C3: FP64 multi-pass FFT N=2^20..2^25, 2 GiB complex128 batch per size per GPU, "
+                         "two_sided_group ABFT on (delta 1e-9)"),
+            "steps": c3["steps"], "ms_per_step": round(c3["ms"], 4),
+            "value": round(world * sum(flops(c["n"], c["b"]) for c in c3["cases"]) / (c3["ms"] / 1000) / 1e9, 1),
+            "unit": "GFLOP/s", "dtype": "f64",
+            "roofline": {"bound": "hbm", "achieved": round(by_exec / t_on / 1e6, 1), "peak": hbm,
+                         "unit": "GB/s", "frac": round(by_exec / t_on / 1e6 / hbm, 4),
+                         "frac_vs_2pass_minimum": round(by_min / t_on / 1e6 / hbm, 4),
+                         "kernel": "fft_pass_kernel<double, L, ...> passes actually launched (+ finalize)"},
+            "abft_overhead_pct": round(100 * (t_on / t_off - 1), 2), "vs_cufft": round(t_cf / t_on, 4),
+            "gpu_launches": int(c3["launches"]), "clocks": c3["clk"],
+            "fault_counters": {"flagged": int(c3["cnt"][0]), "corrected": int(c3["cnt"][1]),
+                               "unrecoverable": int(c3["cnt"][2]), "max_rel_discrepancy": c3["mx"]},
+            "sweep": rows,
+        }
     line = {
         "metric": METRIC,
         "value": round(step_flops / (ms_step / 1000) / 1e9, 1),
@@ -381,66 +517,102 @@ def run_ours(args, rank, world, local_rank):
         "warmup": args.warmup,
         "ms_per_step": round(ms_step, 4),
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong" if args.strong else "weak",
         "vs_baseline": None,
         "dtype": "f32",
         "data": "synthetic (device Philox complex normal), no faults injected",
         "config": {"workload": WORKLOAD, "sizes": [c["n"] for c in cases],
-                   "batch_bytes_per_size_per_gpu": BATCH_BYTES, "scheme": "two_sided_group",
-                   "delta": 1e-4, "parallelism": f"batch-sharded x{world} (no data collective)",
+                   "batch_bytes_per_size_per_gpu": c2_bytes, "scheme": "two_sided_group",
+                   "delta": 1e-4, "parallelism": f"batch-sharded x{world} (NCCL counter all-reduce only)",
                    "l2": "inputs (1 GiB per size) larger than L2 (126 MB); no flush needed"},
         "hbm_gbs": round(achieved, 1),
+        "host_gap_ms_per_step": round(ms_step - tot_on, 4),
         "abft_overhead_pct": round(100 * (tot_on / tot_off - 1), 2),
         "vs_cufft": round(tot_cufft / tot_on, 4),
         "vs_cufft_abft_off": round(tot_cufft / tot_off, 4),
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / hbm, 4),
-                     "traffic": traffic, "traffic_algorithmic": 2 * BATCH_BYTES,
+                     "traffic": traffic, "traffic_algorithmic": 2 * c2_bytes,
                      "kernel": "fft_single_kernel<float, N, ..., ABFT_WANG> (sweep aggregate: "
                                "algorithmic 2*N*8 B per signal / summed event time)"},
         "cpu_baseline": cpu,
         "e2e": e2e,
-        "gpu_launches": len(cases) * args.steps,
+        "gpu_launches": int(launches),
         "clocks": clk,
         "fault_counters": {"flagged": int(counters[0]), "corrected": int(counters[1]),
                            "unrecoverable": int(counters[2]), "recompute": int(counters[3]),
                            "max_rel_discrepancy": max_rel,
-                           "reduced_with": "nccl all_reduce" if world > 1 else "local"},
+                           "reduced_with": "nccl all_reduce per step" if world > 1 else "local"},
         "sweep": sweep,
+        "c3": c3_out,
     }
     print(json.dumps(line), flush=True)
 
 
 def run_reference(args, rank, world):
+    """--impl reference: the reference's CPU implementation of the path (the
+    oracle port with the reference's compiled butterfly) on all host cores,
+    rank 0 only; each step = one all-core wall-timed sample of the C2 sweep."""
     if rank != 0:
         return
-    ms = []
-    vals = []
-    info = None
-    for i in range(args.warmup + args.steps):
-        t0 = time.perf_counter()
-        v, cores, sample, kind = cpu_reference(sample_elems=1 << 21)
-        dt = time.perf_counter() - t0
-        if i >= args.warmup:
-            vals.append(v)
-            ms.append(dt * 1000)
-            info = (cores, sample, kind)
+    import multiprocessing as mp
+    from oracle import port as P
+    kernel = "ref" if P.have_ref_kernel() else "c"
+    cores = os.cpu_count() or 1
+    jobs, fl = _cpu_jobs(1 << 21, cores)
+    jobs = [(a, b, c, kernel) for a, b, c, _ in jobs]
+    ms, vals = [], []
+    with mp.get_context("fork").Pool(cores) as pool:
+        pool.map(_cpu_shard, [(3, 16, 0, kernel)] * cores)
+        for i in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            pool.map(_cpu_shard, jobs, chunksize=1)
+            dt = time.perf_counter() - t0
+            if i >= args.warmup:
+                vals.append(fl / dt / 1e9)
+                ms.append(dt * 1000)
     value = statistics.median(vals)
-    cores, sample, kind = info
+    sample = (f"C2 sweep N=2^3..2^13, 2097152 complex64 samples per size, run_protected "
+              f"two_sided_group, {len(jobs)} group-aligned shards over {cores} processes, pool wall "
+              f"time per step; butterfly: "
+              f"{'reference _stockham compiled from /root/reference (oracle/_ref)' if kernel == 'ref' else 'C restatement'}")
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "GFLOP/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(statistics.median(ms), 2), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "scaling": "strong" if args.strong else "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (numpy default_rng complex normal)",
         "config": {"workload": WORKLOAD, "sizes": [1 << e for e in SIZES],
                    "scheme": "two_sided_group", "delta": 1e-4},
         "cpu_baseline": {"value": round(value, 4), "unit": "GFLOP/s", "cores": cores,
-                         "kind": kind, "sample": sample},
+                         "kind": "port", "sample": sample},
         "e2e": {"value": round(value, 4), "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def _rank_main(rank, world, port, args):
+    """Entry of a self-spawned rank (bench.py --gpus N without torchrun)."""
+    os.environ.update(RANK=str(rank), LOCAL_RANK=str(rank), WORLD_SIZE=str(world),
+                      MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    _run(args, rank, world, rank)
+
+
+def _run(args, rank, world, local_rank):
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    import torch
+    import torch.distributed as dist
+    if world > 1:
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            dist.destroy_process_group()
 
 
 def main():
@@ -449,25 +621,24 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--strong", action="store_true", help="fixed global batch (1 GiB per size) split over the ranks")
     ap.add_argument("--skip-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--skip-c3", action="store_true", help="skip the FP64 C3 leg")
     args = ap.parse_args()
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    if args.impl == "reference":
-        run_reference(args, rank, world)
+    if "WORLD_SIZE" in os.environ:  # torchrun
+        _run(args, int(os.environ.get("RANK", "0")), int(os.environ["WORLD_SIZE"]),
+             int(os.environ.get("LOCAL_RANK", "0")))
         return
-    if world > 1:
-        import torch
-        import torch.distributed as dist
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    try:
-        run_ours(args, rank, world, local_rank)
-    finally:
-        if world > 1:
-            import torch.distributed as dist
-            dist.destroy_process_group()
+    if args.gpus > 1 and args.impl == "ours":
+        import socket
+
+        import torch.multiprocessing as mp
+        with socket.socket() as s:
+            s.bind(("127.0.0.1", 0))
+            port = s.getsockname()[1]
+        mp.spawn(_rank_main, args=(args.gpus, port, args), nprocs=args.gpus, join=True)
+        return
+    _run(args, 0, 1, 0)
 
 
 if __name__ == "__main__":

@@ -128,7 +128,10 @@ def test_c4_campaign_matches_reference(name):
     assert res.recompute_count == ref["recompute"] == 0
     if name == "fp64_exp":  # every fp64 exponent-class flip: detected and corrected (as the reference)
         assert res.detected_count == res.corrected_count == 1000
-    assert stats["compared_detect"] >= 1900 and stats["compared_corrected"] >= 900, stats
+    # every injected run is either compared decision for decision or inside
+    # the x3 band of a threshold (all-bit pools put low-mantissa flips there)
+    assert stats["compared_detect"] + stats["band"] == 1000, stats
+    assert stats["band"] <= (250 if name in ("fp32", "fp64") else 50), stats
 
 
 def test_campaign_exponent_faults_all_detected_and_corrected():

@@ -1,0 +1,151 @@
+"""Parity at the benchmark's own scale (bench.py C2 / C3 batches).
+
+* Every C2 size (fp32 N = 2^3..2^13, 1 GiB batch) and C3 size (fp64
+  N = 2^20..2^25, 2 GiB batch): the protected output equals the unprotected
+  output bitwise (the reference's fusion contract, test_abft.py:265-273), and
+  >= 64 sampled signals (first / last, tile and grid-stride boundaries,
+  random) match an fp64 FFT within 2e-7 (fp32) / 1e-15 (fp64) x log2 n
+  per-signal relative L2.
+* Clean-data flags of the full C2 sweep: every flagged signal's group is
+  re-run through the oracle (the reference restatement with the reference's
+  own compiled butterfly, oracle/_ref) and the reference's relative
+  discrepancy of that signal must not be below delta / 3 (no flag the
+  reference would call clean by a margin). On a random 2^18-sample of every
+  size the decisions of both agree wherever the reference's discrepancy is
+  outside [delta / 3, 3 delta]; the reference's own false-alarm count on the
+  sample is reported (TFFT_SCALE_DUMP=path writes the summary as JSON).
+"""
+
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+C2 = list(range(3, 14))
+C3 = list(range(20, 26))
+
+
+def _plan(n, prec, b):
+    from paper_2405_02520_b200 import make_plan
+    from paper_2405_02520_b200.fft_core import fit_group_size
+    return fit_group_size(make_plan(n, prec, batch=b), b)
+
+
+def _sample_idx(b, rng, k=64):
+    idx = {0, 1, 2, 3, b - 1, b - 2, b - 3}
+    for j in range(1, 24):
+        for e in (148 * j, 148 * 2 * j, 1 << j):  # grid-stride / power-of-two tile boundaries
+            for d in (-1, 0):
+                if 0 <= e + d < b:
+                    idx.add(e + d)
+    idx.update(rng.choice(b, size=min(b, k), replace=False).tolist())
+    return np.array(sorted(i for i in idx if 0 <= i < b))
+
+
+def _run(plan, x, scheme, delta):
+    from paper_2405_02520_b200 import build_twiddles, run_protected
+    from paper_2405_02520_b200.abft import DetectionConfig
+    return run_protected(plan, build_twiddles(plan), x, scheme, DetectionConfig(delta))
+
+
+def _check_size(prec, logn, total_bytes, seed, summary):
+    n = 1 << logn
+    esz = 8 if prec == "fp32" else 16
+    td = torch.complex64 if prec == "fp32" else torch.complex128
+    b = total_bytes // (n * esz)
+    plan = _plan(n, prec, b)
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    x = torch.randn((b, n), dtype=td, device="cuda", generator=g)
+    delta = 1e-4 if prec == "fp32" else 1e-9
+    y_on, rep, _ = _run(plan, x, "two_sided_group", delta)
+    y_off, _, _ = _run(plan, x, "none", delta)
+    assert torch.equal(y_on.view(torch.float32 if prec == "fp32" else torch.float64),
+                       y_off.view(torch.float32 if prec == "fp32" else torch.float64)), (prec, n)
+    del y_off
+    idx = _sample_idx(b, np.random.default_rng([seed, logn]))
+    it = torch.from_numpy(idx).cuda()
+    xs = x.index_select(0, it).cpu().numpy().astype(np.complex128)
+    ys = y_on.index_select(0, it).cpu().numpy().astype(np.complex128)
+    ref = np.fft.fft(xs, axis=1)
+    err = np.linalg.norm(ys - ref, axis=1) / np.linalg.norm(ref, axis=1)
+    tol = (2e-7 if prec == "fp32" else 1e-15) * logn
+    assert err.max() <= tol, (prec, n, float(err.max()), int(idx[err.argmax()]))
+    summary.setdefault("sizes", []).append(
+        {"prec": prec, "n": n, "batch": b, "sampled": len(idx), "max_rel_l2": float(err.max()),
+         "flagged": len(rep.flagged), "unrecoverable": len(rep.unrecoverable),
+         "corrected": len(rep.corrected)})
+    flagged = [(f["signal"], f["discrepancy"]) for f in rep.flagged]
+    xh = None
+    if flagged:
+        sig = torch.tensor(sorted({s for s, _ in flagged}), device="cuda")
+        xh = {int(s): v for s, v in zip(sig.tolist(), x.index_select(0, sig).cpu().numpy())}
+    del x, y_on
+    torch.cuda.empty_cache()
+    return plan, flagged, xh
+
+
+def test_c3_fp64_bench_scale():
+    summary = {}
+    for logn in C3:
+        _check_size("fp64", logn, 2 << 30, 4321, summary)
+    for s in summary["sizes"]:
+        assert s["flagged"] == 0, s  # fp64 clean data: no false alarms at delta 1e-9
+
+
+def _ref_rel(row, kernel):
+    """The reference's rel of one signal: its row through the reference's
+    encode / transform / verify as a group of one (c_in, c_out and the floor
+    are per-signal quantities, pipeline.py:72-135)."""
+    from oracle import port as P
+    n = row.shape[-1]
+    xg = np.asarray(row, dtype=np.complex64)[None, :]
+    enc = P.encoding_for("wang", n, kernel)
+    p1 = P.shrink_bs(P.plan_for(n, "fp32", batch=1), 1)
+    st = P.encode(xg, enc)
+    yg = P.execute(p1, P.twiddles_for(p1), xg.copy(), kernel=kernel)
+    _, rr, _ = P.verify(st, yg, enc, 1e-4, 0.0, "fp32")
+    return float(rr[0])
+
+
+def test_c2_fp32_bench_scale_and_clean_flags_vs_reference():
+    from oracle import port as P
+    kernel = "ref" if P.have_ref_kernel() else "c"
+    summary = {"kernel": kernel}
+    flags = []
+    for logn in C2:
+        plan, flagged, xh = _check_size("fp32", logn, 1 << 30, 1234, summary)
+        n = 1 << logn
+        for s, rel in flagged:
+            flags.append({"n": n, "signal": int(s), "rel_ours": float(rel),
+                          "rel_reference": _ref_rel(xh[s], kernel)})
+    summary["clean_flags"] = flags
+    for f in flags:
+        assert f["rel_reference"] > 1e-4 / 3, f  # a flag the reference would call clean: fail
+    summary["flags_reference_also_flags"] = sum(f["rel_reference"] > 1e-4 for f in flags)
+    # random sample of every size: decisions agree outside the x3 band
+    rng = np.random.default_rng(99)
+    sample = []
+    for logn in C2:
+        n = 1 << logn
+        b = max(16, (1 << 18) // n) // 16 * 16
+        x = (rng.standard_normal((b, n)) + 1j * rng.standard_normal((b, n))).astype(np.complex64)
+        plan = _plan(n, "fp32", b)
+        _, rep, _ = _run(plan, torch.from_numpy(x).cuda(), "two_sided_group", 1e-4)
+        mine = {f["signal"] for f in rep.flagged}
+        op = P.shrink_bs(P.plan_for(n, "fp32", batch=b), plan.bs)
+        _, orep, _ = P.protected(op, P.twiddles_for(op), x, "two_sided_group", delta=1e-4,
+                                 enc=P.encoding_for("wang", n, kernel), kernel=kernel)
+        theirs = {f["signal"]: f["discrepancy"] for f in orep["flagged"]}
+        for s in mine ^ set(theirs):
+            r = theirs[s] if s in theirs else _ref_rel(x[s], kernel)
+            assert 1e-4 / 3 < r < 3e-4, (n, s, r)
+        sample.append({"n": n, "signals": b, "ours_flagged": len(mine), "reference_flagged": len(theirs)})
+    summary["random_sample"] = sample
+    dump = os.environ.get("TFFT_SCALE_DUMP")
+    if dump:
+        with open(dump, "w") as f:
+            json.dump(summary, f, indent=1)

@@ -1,0 +1,211 @@
+"""C4: the fault campaigns at their stated size on the B200, and
+the online-correction overhead.
+
+    python tools/c4.py [--out gpurun_out/c4.json]
+
+1. `run_campaign(CampaignConfig(runs=2000, inject_fraction=0.5, n=2**16,
+   batch=16, precision=p, seed=1))` for fp32 / fp64 and the exponent-class
+   pools (bits 25-30 / 57-62). For each: detection and correction rates at
+   the calibrated delta (all injected runs, exponent-class runs, sub-threshold
+   rate), device time, and the record-by-record agreement with the REAL
+   reference's CSVs (tests/golden/c4_*): decisions compared wherever the
+   reference's discrepancy is outside x3 of the threshold.
+2. Online correction overhead t(faulty) / t(clean) - 1 of the protected call
+   (CUDA events around the whole call: fused launch, detection read-back,
+   correction, verdict) on a 1 GiB batch of the C4 shape (N = 2^16, bs 16,
+   128 groups): one fault in the launch (the paper's "under error injection",
+   PAPER.md:472) and one fault in EVERY group (tfft_run_campaign fault table).
+SM clocks are sampled during every timed region.
+"""
+
+from __future__ import annotations
+
+import argparse
+import csv
+import ctypes
+import json
+import os
+import statistics
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from bench import ClockSampler  # noqa: E402
+
+GOLD = os.path.join(ROOT, "tests", "golden")
+
+
+def agreement(res, name):
+    from paper_2405_02520_b200.fault_lab import records_csv
+    import io
+    mine = list(csv.DictReader(io.StringIO(records_csv(res))))
+    ref = list(csv.DictReader(open(os.path.join(GOLD, f"c4_{name}_records.csv"))))
+    clean_ref = [float(r["discrepancy"]) for r in ref if r["injected"] == "0"]
+    ref_dd = 10.0 * float(np.quantile(clean_ref, 0.999))
+    same_run = all(m[k] == r[k] for m, r in zip(mine, ref)
+                   for k in ("run_id", "injected", "signal_idx", "element_idx", "bit"))
+    cmp_ = agree = band = 0
+    cor_cmp = cor_agree = 0
+    op = 1e-4 if res.config.precision == "fp32" else 1e-9
+    for m, r in zip(mine, ref):
+        if r["injected"] != "1":
+            continue
+        dr = float(r["discrepancy"])
+        if (ref_dd / 3 < dr < 3 * ref_dd) or (res.default_delta / 3 < dr < 3 * res.default_delta):
+            band += 1
+            continue
+        cmp_ += 1
+        agree += m["detected_at_default_delta"] == r["detected_at_default_delta"]
+        if not (op / 3 < dr < 3 * op):
+            cor_cmp += 1
+            cor_agree += m["corrected"] == r["corrected"]
+    return {"same_runs_and_faults": same_run, "decisions_compared": cmp_, "decisions_equal": agree,
+            "near_threshold_band": band, "corrected_compared": cor_cmp, "corrected_equal": cor_agree,
+            "reference_default_delta": ref_dd}
+
+
+def rates(res, bits_exp):
+    recs = [r for r in res.records if r.injected]
+    det = [r.discrepancy > res.default_delta for r in recs]
+    exp = [(d, r.corrected) for d, r in zip(det, recs) if r.bit in bits_exp]
+    return {
+        "injected": len(recs),
+        "detection_rate": sum(det) / len(recs),
+        "corrected_rate": sum(d and r.corrected for d, r in zip(det, recs)) / len(recs),
+        "subthreshold_rate": 1 - sum(det) / len(recs),
+        "exponent_class_runs": len(exp),
+        "exponent_class_detection_rate": (sum(d for d, _ in exp) / len(exp)) if exp else None,
+        "exponent_class_corrected_rate": (sum(d and c for d, c in exp) / len(exp)) if exp else None,
+        "corrected_fraction_of_detected": res.corrected_fraction_of_detected(),
+    }
+
+
+def campaigns(out):
+    from paper_2405_02520_b200.fault_lab import CampaignConfig, run_campaign
+    c4 = json.load(open(os.path.join(GOLD, "c4_summary.json")))
+    for name in ("fp32", "fp64", "fp32_exp", "fp64_exp"):
+        kw = dict(c4["config"], **c4["variants"][name])
+        if "bits" in kw:
+            kw["bits"] = tuple(kw["bits"])
+        bits_exp = set(range(25, 31)) if kw["precision"] == "fp32" else set(range(57, 63))
+        clk = ClockSampler(0)
+        clk.start()
+        t0 = time.perf_counter()
+        res = run_campaign(CampaignConfig(**kw))
+        wall = time.perf_counter() - t0
+        ref = c4[name]
+        out["campaigns"][name] = {
+            "config": {k: (list(v) if isinstance(v, tuple) else v) for k, v in kw.items()},
+            "default_delta": res.default_delta,
+            "detected": res.detected_count, "corrected": res.corrected_count,
+            "recompute": res.recompute_count,
+            **rates(res, bits_exp),
+            "reference": {"default_delta": ref["default_delta"], "detected": ref["detected"],
+                          "corrected": ref["corrected"], "recompute": ref["recompute"],
+                          "cpu_seconds_one_core": ref["seconds"]},
+            "agreement_with_reference": agreement(res, name),
+            "device_ms": {"protected": round(res.timing["protected_ms"], 2),
+                          "clean_reruns": round(res.timing["clean_ms"], 2)},
+            "wall_s": round(wall, 2), "clocks": clk.stop(),
+        }
+        print(name, json.dumps(out["campaigns"][name]["agreement_with_reference"]), flush=True)
+
+
+def overhead(out, reps=20):
+    import torch
+
+    from paper_2405_02520_b200 import _lib, make_plan
+    from paper_2405_02520_b200.abft import make_encoding
+    from paper_2405_02520_b200.fft_core import fit_group_size
+    from paper_2405_02520_b200.fft_core.plan import native_plan
+    lib = _lib.load()
+    for prec in ("fp32", "fp64"):
+        n, bs = 1 << 16, 16
+        esz = 8 if prec == "fp32" else 16
+        td = torch.complex64 if prec == "fp32" else torch.complex128
+        b = (1 << 30) // (n * esz)
+        runs = b // bs
+        plan = fit_group_size(make_plan(n, prec, batch=bs), bs)
+        h = native_plan(plan, 0)
+        row = make_encoding("wang", n).device_row(td, False)
+        x = torch.randn(b, n, dtype=td, device="cuda")
+        y = torch.empty_like(x)
+        delta = 1e-4 if prec == "fp32" else 1e-9
+        bit = 30 if prec == "fp32" else 62
+        rng = np.random.default_rng(3)
+        every = (_lib.Fault * runs)()
+        for r in range(runs):
+            f = every[r]
+            f.signal, f.element = int(rng.integers(bs)), int(rng.integers(n))
+            f.component, f.bit, f.where = int(rng.integers(2)), bit, _lib.AT_OUTPUT
+        one = (_lib.Fault * runs)()
+        for r in range(runs):
+            one[r].where = _lib.AT_NONE
+        one[runs // 2] = every[runs // 2]
+        clean = (_lib.Fault * runs)()
+        for r in range(runs):
+            clean[r].where = _lib.AT_NONE
+        run_max = (ctypes.c_double * runs)()
+        fired = (ctypes.c_int32 * runs)()
+        rep = _lib.Report()
+        cap = 4096
+        keep = ((_lib.Flag * cap)(), (ctypes.c_int64 * cap)(), (ctypes.c_int64 * cap)(), (ctypes.c_int64 * cap)())
+        rep.flagged, rep.flagged_cap = keep[0], cap
+        rep.corrected_group, rep.corrected_signal, rep.corrected_cap = keep[1], keep[2], cap
+        rep.unrecoverable, rep.unrecoverable_cap = keep[3], cap
+        stream = torch.cuda.current_stream()
+
+        def call(faults):
+            _lib.check(lib.tfft_run_campaign(h.handle, x.data_ptr(), y.data_ptr(), runs, bs,
+                                             _lib.SCHEME_CODE["two_sided_group"], delta, 0.0, row.data_ptr(),
+                                             None, faults, 0, run_max, fired, ctypes.byref(rep),
+                                             stream.cuda_stream), "tfft_run_campaign")
+
+        res = {}
+        clk = ClockSampler(0)
+        for label, faults in (("clean", clean), ("one_fault_per_launch", one), ("one_fault_per_group", every)):
+            for _ in range(3):
+                call(faults)
+            ts = []
+            clk.start() if label == "clean" else None
+            for _ in range(reps):
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                call(faults)
+                e1.record(stream)
+                torch.cuda.synchronize()
+                ts.append(e0.elapsed_time(e1))
+            res[label] = {"ms": round(statistics.median(ts), 4), "corrected": int(rep.n_corrected),
+                          "unrecoverable": int(rep.n_unrecoverable), "flagged": int(rep.n_flagged)}
+        res["clocks"] = clk.stop()
+        for k in ("one_fault_per_launch", "one_fault_per_group"):
+            res[k]["overhead_pct"] = round(100 * (res[k]["ms"] / res["clean"]["ms"] - 1), 2)
+        res["shape"] = {"n": n, "bs": bs, "groups": runs, "bytes": b * n * esz,
+                        "call": "tfft_run_campaign (fused launch + per-run max rel read-back + correction)",
+                        "fault": f"output bit {bit}, random signal/element/component per group"}
+        out["correction_overhead"][prec] = res
+        print(prec, json.dumps({k: v for k, v in res.items() if k != "clocks"}), flush=True)
+        del x, y
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "c4.json"))
+    args = ap.parse_args()
+    import torch
+    torch.cuda.set_device(0)
+    out = {"campaigns": {}, "correction_overhead": {}}
+    campaigns(out)
+    overhead(out)
+    os.makedirs(os.path.dirname(args.out), exist_ok=True)
+    with open(args.out, "w") as f:
+        json.dump(out, f, indent=1)
+
+
+if __name__ == "__main__":
+    main()
