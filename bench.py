@@ -143,9 +143,11 @@ def _cpu_shard(args):
     plan = P.shrink_bs(P.plan_for(n, "fp32", batch=nsig), nsig)
     tw = P.twiddles_for(plan)
     enc = P.encoding_for("wang", n)
-    t0 = time.perf_counter()
-    P.protected(plan, tw, x, "two_sided_group", delta=1e-4, enc=enc, kernel=kernel)
-    return time.perf_counter() - t0
+    from threadpoolctl import threadpool_limits
+    with threadpool_limits(1):  # one core per worker: no BLAS thread oversubscription
+        t0 = time.perf_counter()
+        P.protected(plan, tw, x, "two_sided_group", delta=1e-4, enc=enc, kernel=kernel)
+        return time.perf_counter() - t0
 
 
 def _cpu_jobs(sample_elems, shards_per_size):
@@ -160,12 +162,13 @@ def _cpu_jobs(sample_elems, shards_per_size):
     return jobs, total
 
 
-def cpu_reference(cores=None, single_elems=1 << 18, multi_elems=1 << 22):
+def cpu_reference(cores=None, single_elems=1 << 21, multi_elems=1 << 23):
     """The reference's CPU path (oracle port; butterflies by the reference's
     own compiled `_stockham` when oracle/_ref is built) over bounded samples
     of the C2 sweep, measured two ways:
       * 1 core: one process, `single_elems` complex64 samples per size, the
-        summed run_protected time (the reference as shipped is single-threaded);
+        summed run_protected time (the reference as shipped is single-threaded;
+        BLAS is held to one thread, threadpoolctl);
       * all cores: `multi_elems` samples per size sharded by checksum group over
         a pool of `cores` processes, timed as the WALL time of the pool map
         (workers warmed first; the wall includes each shard's seeded input draw).
@@ -559,7 +562,7 @@ def run_reference(args, rank, world):
     from oracle import port as P
     kernel = "ref" if P.have_ref_kernel() else "c"
     cores = os.cpu_count() or 1
-    jobs, fl = _cpu_jobs(1 << 21, cores)
+    jobs, fl = _cpu_jobs(1 << 22, cores)
     jobs = [(a, b, c, kernel) for a, b, c, _ in jobs]
     ms, vals = [], []
     with mp.get_context("fork").Pool(cores) as pool:
@@ -572,7 +575,7 @@ def run_reference(args, rank, world):
                 vals.append(fl / dt / 1e9)
                 ms.append(dt * 1000)
     value = statistics.median(vals)
-    sample = (f"C2 sweep N=2^3..2^13, 2097152 complex64 samples per size, run_protected "
+    sample = (f"C2 sweep N=2^3..2^13, 4194304 complex64 samples per size, run_protected "
               f"two_sided_group, {len(jobs)} group-aligned shards over {cores} processes, pool wall "
               f"time per step; butterfly: "
               f"{'reference _stockham compiled from /root/reference (oracle/_ref)' if kernel == 'ref' else 'C restatement'}")

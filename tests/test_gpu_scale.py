@@ -63,10 +63,17 @@ def _check_size(prec, logn, total_bytes, seed, summary):
     delta = 1e-4 if prec == "fp32" else 1e-9
     y_on, rep, _ = _run(plan, x, "two_sided_group", delta)
     y_off, _, _ = _run(plan, x, "none", delta)
-    assert torch.equal(y_on.view(torch.float32 if prec == "fp32" else torch.float64),
-                       y_off.view(torch.float32 if prec == "fp32" else torch.float64)), (prec, n)
+    # fusion contract: bitwise equal except the signals a (clean-data) flag
+    # got corrected: those were rebuilt as W s0 - sum of the others and
+    # re-verified (pipeline.py:180-191), equal to the FFT only to rounding
+    fixed = sorted({c["signal"] for c in rep.corrected})
+    rv = torch.float32 if prec == "fp32" else torch.float64
+    keep = torch.ones(b, dtype=torch.bool, device="cuda")
+    if fixed:
+        keep[torch.tensor(fixed, device="cuda")] = False
+    assert torch.equal(y_on[keep].view(rv), y_off[keep].view(rv)), (prec, n)
     del y_off
-    idx = _sample_idx(b, np.random.default_rng([seed, logn]))
+    idx = np.union1d(_sample_idx(b, np.random.default_rng([seed, logn])), np.array(fixed, dtype=np.int64))
     it = torch.from_numpy(idx).cuda()
     xs = x.index_select(0, it).cpu().numpy().astype(np.complex128)
     ys = y_on.index_select(0, it).cpu().numpy().astype(np.complex128)
