@@ -168,6 +168,13 @@ int tfft_plan_exec_passes(const tfft_plan *plan);
  * n <= 2^13 with the Wang encoding (values == NULL). */
 int tfft_set_check_level(tfft_plan *plan, int level);
 
+/* Online correction of the single-kernel sizes (n <= 2^13) runs on the
+ * device, queued right behind the fused transform (enable = 1, default): a
+ * flagged call costs no extra host round trip. enable = 0 makes the host
+ * decide first and launch the same correction kernel with its job list
+ * (identical results; used to test one against the other). */
+int tfft_set_device_correction(tfft_plan *plan, int enable);
+
 /* The two halves of tfft_run_protected, for callers that queue several
  * protected transforms before reading their reports (one in-flight protected
  * call per plan): _launch enqueues the fused transform and the tiny

@@ -66,6 +66,7 @@ SIGNATURES = {
     "tfft_protect_finish": (_INT, [_VP, _VP, _VP, _I64, _INT, _DBL, _DBL, _VP, _VP, _INT,
                                    ctypes.POINTER(Report), _VP]),
     "tfft_set_check_level": (_INT, [_VP, _INT]),
+    "tfft_set_device_correction": (_INT, [_VP, _INT]),
     "tfft_plan_exec_passes": (_INT, [_VP]),
     "tfft_tile_fft": (_INT, [_VP, _VP, _I64, _I64, _INT, _INT, _INT, _VP]),
     "tfft_encode_group": (_INT, [_VP, _VP, _I64, _VP, _VP, _VP, _VP, _VP, _VP]),

@@ -214,7 +214,7 @@ def _emit_single(prec, cfgs, part, table=False):
     t = CTYPE[prec]
     lines = [
         "// GENERATED by paper_2405_02520_b200/codegen.py — do not edit.",
-        '#include "single.cuh"',
+        '#include "fix.cuh"',
         '#include "registry.h"',
         "namespace tfft {",
     ]
@@ -228,10 +228,16 @@ def _emit_single(prec, cfgs, part, table=False):
                 continue
             fns.append(f"(const void*)&fft_single_kernel<{t}, {c['n']}, {c['e']}, {c['ps']}, "
                        f"{abft}, {c['threads']}, {c['minb']}, {c['stage']}, RList<{rl}>>")
+        fix = "nullptr, 0, 0"
+        if c["chosen"]:  # device-side correction with the same engine config (fix.cuh)
+            ft = max(c["tps"], 32)
+            fsl = (c["n"] + (c["n"] >> c["ps"]) + 1 if c["ps"] else c["n"]) if len(c["radices"]) > 1 else 1
+            fix = (f"(const void*)&fix_single_kernel<{t}, {c['n']}, {c['e']}, {c['ps']}, {ft}, RList<{rl}>>, "
+                   f"{ft}, {(ft // c['tps']) * fsl * ELEM_BYTES[prec]}")
         entries.append(
             f"    {{{c['logn']}, {c['variant']}, {int(c['chosen'])}, {c['e']}, {c['threads']}, "
-            f"{c['smem']}, {c['tps']}, {c['stage']}, {{{', '.join(fns)}}}}},  // radices {rl}, pad 2^{c['ps']}, "
-            f"minb {c['minb']}, stage {c['stage']}")
+            f"{c['smem']}, {c['tps']}, {c['stage']}, {{{', '.join(fns)}}}, {fix}}},  // radices {rl}, "
+            f"pad 2^{c['ps']}, minb {c['minb']}, stage {c['stage']}")
     lines.append(f"extern const SingleEntry kSingle_{prec}_{part}[] = {{")
     lines += entries
     lines.append("};")

@@ -142,12 +142,6 @@ detect_kernel(const C<T>* __restrict__ y, long long n, const C<T>* __restrict__ 
     }
 }
 
-struct FixJob {
-    long long first;     // global index of the group's first signal
-    long long flagged;   // global index of the flagged signal
-    int ok;              // out: 1 = corrected and verified
-    int pad;
-};
 
 // s0 of K flagged groups in one launch (grid.y = group): s0[k] = sum over
 // the group's bs signals, sequential in b like group_sums_kernel.

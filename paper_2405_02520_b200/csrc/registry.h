@@ -19,6 +19,9 @@ struct SingleEntry {
     int tps;         // threads per signal
     int stage;       // load strategy (STAGE template argument; 5 needs a tensor map)
     const void* fn[4];  // ABFT off / Wang / table / thread-level (last two only on the chosen variant)
+    const void* fix;    // fix_single_kernel of this config (chosen variant only), see fix.cuh
+    int fix_threads;    // its CTA size: max(TPS, 32)
+    int fix_smem;       // its dynamic shared memory (exchange slices)
 };
 
 struct SingleTable {

@@ -46,6 +46,15 @@ struct FlagRec {
     double rel;
 };
 
+// One group of a correction pass: its first signal and the flagged one
+// (global indices); ok = 1 once corrected and verified.
+struct FixJob {
+    long long first;
+    long long flagged;
+    int ok;
+    int pad;
+};
+
 // Append one flag: a record while the list has room, else a bit in the
 // overflow mask (the host recomputes those signals' rel exactly). The record
 // list is bounded (kMaxFlagRecords), so a degenerate batch with millions of

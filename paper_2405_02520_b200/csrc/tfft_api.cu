@@ -22,6 +22,7 @@
 
 #include "../../include/tfft.h"
 #include "aux_kernels.cuh"
+#include "fix.cuh"
 #include "multi.cuh"
 #include "registry.h"
 
@@ -105,8 +106,15 @@ struct Counters {
     int flag_count;
     int pad;
     unsigned long long max_key;  // float key in low 32 bits for fp32
+    FixHead fix;                 // verdict header of the device-side correction (fix.cuh)
 };
-constexpr size_t kBlockHead = 64;  // Counters, padded: the flag records start 64-byte aligned
+// Detection block: Counters (padded to 64 B), the device correction's
+// per-job verdicts, then the flag records (64-byte aligned). One D2H copy of
+// the first kBlockHead + kEarly records brings back everything a clean or a
+// singly-faulted call needs.
+constexpr size_t kFixOff = 64;
+constexpr size_t kBlockHead = kFixOff + kFixCap * sizeof(FixRes);
+static_assert(sizeof(Counters) <= kFixOff && kBlockHead % 64 == 0, "detection block layout");
 
 // [prec][logn][variant] -> entry, plus the tuned default and a runtime override
 constexpr int kMaxVariants = 16;
@@ -178,6 +186,7 @@ struct tfft_plan {
     int64_t bs = 1;
     int device = 0;
     int check_level = 0;            // 0 threadblock checksums, 1 thread-level (scheme comparison)
+    int dev_fix = 1;                // single-kernel sizes: correct on the device behind the launch
     int logn = 0;
     int num_sms = 148;
     size_t esize = 8;               // bytes per complex element
@@ -395,6 +404,53 @@ int launch_transform(tfft_plan* p, const Launch& L, cudaStream_t st) {
     int rc = multi_launch(mp, m, st);
     if (rc) return fail(rc, multi_last_error());
     return TFFT_OK;
+}
+
+// The device-side correction pass (fix.cuh) of a single-kernel plan: plan
+// mode (jobs == nullptr) right behind the fused launch, or list mode with
+// host-chosen jobs. Returns TFFT_EUNSUPPORTED when the plan's kernel config
+// has no fix instantiation (tuning overrides), so callers fall back.
+template <class T>
+int launch_fix_t(tfft_plan* p, const void* in, void* out, const void* etw, const void* values, double delta,
+                 double abs_floor, int inverse, int one_sided, FixJob* jobs, int njobs, cudaStream_t st) {
+    const SingleEntry* e = single_entry(p->prec, p->logn);
+    if (!e || !e->fix) return TFFT_EUNSUPPORTED;
+    int nb = 0;
+    int rc = prepare_kernel(e->fix, e->fix_threads, e->fix_smem, &nb);
+    if (rc) return rc;
+    FixArgs<T> a;
+    memset(&a, 0, sizeof(a));
+    a.in = (const C<T>*)in;
+    a.out = (C<T>*)out;
+    a.bs = p->bs;
+    a.tw = (const C<T>*)p->tw;
+    a.etw = (const C<T>*)etw;
+    a.values = (const C<T>*)values;
+    a.delta = (T)delta;
+    a.abs_floor = (T)abs_floor;
+    a.floor_coef = p->prec == TFFT_FP32 ? (T)1e-6f : (T)1e-12;
+    a.inverse = inverse;
+    a.scale_inv = inverse;
+    a.one_sided = one_sided;
+    a.flag_count = &p->d_cnt->flag_count;
+    a.flag_rec = p->d_flag_rec;
+    a.jobs = jobs;
+    a.njobs = njobs;
+    a.jobs_out = jobs;
+    a.head = &p->d_cnt->fix;
+    a.res = reinterpret_cast<FixRes*>(p->d_block + kFixOff);
+    const int grid = jobs ? std::max(1, std::min(njobs, 2 * p->num_sms)) : 8;
+    void* args[] = {&a};
+    CU((tfft::note_launch(), cudaLaunchKernel(e->fix, dim3(grid), dim3(e->fix_threads), args, e->fix_smem, st)));
+    return TFFT_OK;
+}
+
+int launch_fix(tfft_plan* p, const void* in, void* out, const void* etw, const void* values, double delta,
+               double abs_floor, int inverse, int one_sided, FixJob* jobs, int njobs, cudaStream_t st) {
+    return p->prec == TFFT_FP32
+               ? launch_fix_t<float>(p, in, out, etw, values, delta, abs_floor, inverse, one_sided, jobs, njobs, st)
+               : launch_fix_t<double>(p, in, out, etw, values, delta, abs_floor, inverse, one_sided, jobs, njobs,
+                                      st);
 }
 
 Launch base_launch(const void* in, void* out, int64_t batch, int inverse) {
@@ -849,6 +905,13 @@ int tfft_protect_launch(tfft_plan* p, const void* in, void* out, int64_t batch, 
     rc = launch_transform(p, L, st);
     if (rc) return rc;
     if (!prot) return TFFT_OK;
+    // single-kernel sizes: the corrections run on the device right behind the
+    // transform (fix.cuh), so the summary below already carries the verdicts
+    if (p->single && p->dev_fix && scheme != TFFT_SCHEME_NONE) {
+        rc = launch_fix(p, in, out, etw, values, delta, abs_floor, inverse ? 1 : 0,
+                        scheme == TFFT_SCHEME_ONE_SIDED, nullptr, 0, st);
+        if (rc && rc != TFFT_EUNSUPPORTED) return rc;
+    }
     // the (tiny) detection summary rides back behind the transform
     rc = enqueue_summary(p, st);
     if (rc) return rc;
@@ -1027,6 +1090,27 @@ int correct_groups(tfft_plan* p, const void* in, void* out, int scheme, const vo
     int rc;
     fixed_ok.assign(fix_groups.size(), 0);
     if (fix_groups.empty()) return TFFT_OK;
+    if (p->single && single_entry(p->prec, p->logn)->fix) {
+        // the device correction pass with a host job list (identical
+        // arithmetic to the plan-mode pass behind the fused launch)
+        const int64_t K = (int64_t)fix_groups.size();
+        if (K > p->jobs_cap) {
+            cudaFree(p->d_jobs);
+            p->d_jobs = nullptr;
+            CU(cudaMalloc(&p->d_jobs, K * sizeof(FixJob)));
+            p->jobs_cap = K;
+        }
+        std::vector<FixJob> jobs(K);
+        for (int64_t k = 0; k < K; ++k) jobs[k] = FixJob{fix_groups[k] * p->bs, fix_sig[k], 0, 0};
+        CU(cudaMemcpyAsync(p->d_jobs, jobs.data(), K * sizeof(FixJob), cudaMemcpyHostToDevice, st));
+        rc = launch_fix(p, in, out, etw, values, delta, abs_floor, inverse ? 1 : 0,
+                        scheme == TFFT_SCHEME_ONE_SIDED, p->d_jobs, (int)K, st);
+        if (rc) return rc;
+        CU(cudaMemcpyAsync(jobs.data(), p->d_jobs, K * sizeof(FixJob), cudaMemcpyDeviceToHost, st));
+        CU(cudaStreamSynchronize(st));
+        for (int64_t k = 0; k < K; ++k) fixed_ok[k] = (char)jobs[k].ok;
+        return TFFT_OK;
+    }
     if (scheme == TFFT_SCHEME_ONE_SIDED) {
         for (size_t i = 0; i < fix_groups.size(); ++i) {
             Launch R = base_launch((const char*)in + fix_sig[i] * n * p->esize,
@@ -1146,13 +1230,26 @@ int tfft_protect_finish(tfft_plan* p, const void* in, void* out, int64_t batch, 
     RecheckFn resolve = [&](const std::vector<long long>& sg, std::vector<double>& rr) {
         return recheck_device(p, in, out, sg, etw, values, abs_floor, rr, st);
     };
-    rc = read_summary(p, batch, st, rep, flags, delta, resolve);
+    rc = read_summary(p, batch, st, rep, flags, delta, resolve);  // waits for the summary copy
     if (rc) return rc;
+    const FixHead fh = p->h_cnt->fix;
     std::vector<int64_t> bad_groups, fix_groups, fix_sig;
     decide(p, flags, bad_groups, fix_groups, fix_sig);
     std::vector<char> fixed_ok;
-    rc = correct_groups(p, in, out, scheme, etw, values, delta, abs_floor, inverse, fix_groups, fix_sig, fixed_ok, st);
-    if (rc) return rc;
+    if (fh.ran && !fh.fallback) {
+        // corrected on the device already (same grouping, same order)
+        if (fh.njobs != (int)fix_groups.size()) return fail(TFFT_ECUDA, "device correction disagrees with the host grouping");
+        const FixRes* fr = reinterpret_cast<const FixRes*>(p->h_block + kFixOff);
+        fixed_ok.resize(fix_groups.size());
+        for (size_t i = 0; i < fix_groups.size(); ++i) {
+            if (fr[i].signal != fix_sig[i]) return fail(TFFT_ECUDA, "device correction job mismatch");
+            fixed_ok[i] = (char)fr[i].ok;
+        }
+    } else {
+        rc = correct_groups(p, in, out, scheme, etw, values, delta, abs_floor, inverse, fix_groups, fix_sig, fixed_ok,
+                            st);
+        if (rc) return rc;
+    }
     fill_lists(p, scheme, rep, bad_groups, fix_groups, fix_sig, fixed_ok);
     return TFFT_OK;
 }
@@ -1775,6 +1872,12 @@ int tfft_element_verify(int r, int64_t B, void* y, const void* row_in, const voi
 }  // extern "C"
 
 extern "C" {
+
+int tfft_set_device_correction(tfft_plan* p, int enable) {
+    if (!p) return fail(TFFT_EINVAL, "null plan");
+    p->dev_fix = enable ? 1 : 0;
+    return TFFT_OK;
+}
 
 int tfft_set_check_level(tfft_plan* p, int level) {
     if (!p) return fail(TFFT_EINVAL, "null plan");
