@@ -61,16 +61,19 @@ SINGLE_CANDIDATES = {
         11: _cands((16, (16, 16, 8), 256, 2, 0), (16, (16, 16, 8), 256, 3, 0),
                    (8, (8, 8, 8, 4), 256, 3, 0), (16, (16, 16, 8), 512, 1, 0),
                    (16, (16, 16, 8), 256, 3, 2), (16, (16, 16, 8), 256, 2, 2),
-                   (16, (16, 16, 8), 256, 2, 4), (32, (32, 32, 2), 128, 3, 0), (32, (32, 16, 4), 128, 3, 0)),
+                   (16, (16, 16, 8), 256, 2, 4), (32, (32, 32, 2), 128, 3, 0), (32, (32, 16, 4), 128, 3, 0),
+                   (32, (32, 16, 4), 128, 2, 6), (32, (32, 32, 2), 128, 2, 6), (16, (16, 16, 8), 256, 2, 6)),
         12: _cands((16, (16, 16, 16), 256, 2, 0), (16, (16, 16, 16), 256, 3, 0),
                    (8, (8, 8, 8, 8), 512, 2, 0), (16, (16, 16, 16), 512, 1, 0),
                    (16, (16, 16, 16), 256, 3, 2), (16, (16, 16, 16), 256, 2, 2),
-                   (16, (16, 16, 16), 256, 2, 4), (32, (32, 32, 4), 128, 3, 0), (32, (32, 16, 8), 128, 3, 0)),
+                   (16, (16, 16, 16), 256, 2, 4), (32, (32, 32, 4), 128, 3, 0), (32, (32, 16, 8), 128, 3, 0),
+                   (16, (16, 16, 16), 256, 2, 6), (32, (32, 16, 8), 128, 2, 6)),
         13: _cands((16, (16, 16, 16, 2), 512, 2, 0), (32, (32, 16, 16), 256, 1, 0),
                    (16, (16, 16, 16, 2), 512, 1, 0), (8, (8, 8, 8, 8, 2), 1024, 1, 0),
                    (16, (16, 16, 16, 2), 512, 2, 2), (16, (16, 16, 16, 2), 512, 1, 2),
                    (16, (16, 16, 16, 2), 512, 2, 1), (16, (16, 16, 16, 2), 512, 2, 4),
-                   (16, (16, 16, 16, 2), 512, 1, 4)),
+                   (16, (16, 16, 16, 2), 512, 1, 4), (16, (16, 16, 16, 2), 512, 1, 6),
+                   (32, (32, 16, 16), 256, 1, 6), (32, (32, 16, 16), 256, 1, 4)),
     },
     "fp64": {
         1: _cands((2, (2,), 256, 1, 1), (2, (2,), 256, 1, 0), (2, (2,), 256, 1, 3)),
@@ -97,11 +100,12 @@ SINGLE_CANDIDATES = {
                    (16, (16, 16, 4), 128, 2, 0)),
         11: _cands((16, (16, 16, 8), 256, 1, 0), (16, (16, 16, 8), 256, 2, 0),
                    (8, (8, 8, 8, 4), 256, 2, 0), (16, (16, 16, 8), 256, 2, 2),
-                   (8, (8, 8, 8, 4), 256, 2, 4), (16, (16, 16, 8), 128, 3, 0), (16, (16, 16, 8), 128, 2, 0)),
+                   (8, (8, 8, 8, 4), 256, 2, 4), (16, (16, 16, 8), 128, 3, 0), (16, (16, 16, 8), 128, 2, 0),
+                   (16, (16, 16, 8), 256, 1, 6), (16, (16, 16, 8), 128, 1, 6)),
         12: _cands((16, (16, 16, 16), 256, 1, 0), (16, (16, 16, 16), 512, 1, 0),
                    (8, (8, 8, 8, 8), 512, 1, 0), (16, (16, 16, 16), 256, 1, 2),
                    (16, (16, 16, 16), 256, 1, 4), (8, (8, 8, 8, 8), 512, 1, 4),
-                   (8, (8, 8, 8, 8), 512, 2, 4)),
+                   (8, (8, 8, 8, 8), 512, 2, 4), (16, (16, 16, 16), 256, 1, 6)),
         13: _cands((16, (16, 16, 16, 2), 512, 1, 0), (8, (8, 8, 8, 8, 2), 1024, 1, 0),
                    (16, (16, 16, 16, 2), 512, 1, 4), (8, (8, 8, 8, 8, 2), 1024, 1, 4)),
     },
@@ -179,14 +183,28 @@ def choose_padding(n, e, radices, prec):
     return best
 
 
+def tune_sizes():
+    """TFFT_TUNE_SIZES="fp32:11,12,13;fp64:12" limits the tuning build's extra
+    candidates to those sizes (every other size keeps its chosen kernel)."""
+    spec = os.environ.get("TFFT_TUNE_SIZES", "")
+    if not spec:
+        return None
+    out = set()
+    for part in spec.split(";"):
+        prec, sizes = part.split(":")
+        out.update((prec, int(v)) for v in sizes.split(","))
+    return out
+
+
 def single_configs(all_candidates=True):
     """Every candidate (all_candidates) or only the chosen one per size."""
     out = []
+    only = tune_sizes() if all_candidates else None
     for prec, table in SINGLE_CANDIDATES.items():
         for logn, cands in sorted(table.items()):
             chosen = SINGLE_CHOICE[prec].get(logn, 0)
             for vi, c in enumerate(cands):
-                if not all_candidates and vi != chosen:
+                if (not all_candidates or (only is not None and (prec, logn) not in only)) and vi != chosen:
                     continue
                 n = 1 << logn
                 e, radices = c["e"], c["radices"]
@@ -197,13 +215,14 @@ def single_configs(all_candidates=True):
                 s = threads // tps
                 ex = (n + (n >> ps) + 1 if ps else n) if len(radices) > 1 else 0
                 st = n + 1 if c["stage"] in (1, 3) else (n if c["stage"] == 4 else 0)
-                ib = s * n if c["stage"] in (2, 3) else 0  # TMA prefetch buffer
+                ib = s * n if c["stage"] in (2, 3, 6) else 0  # TMA prefetch buffer
                 if c["stage"] == 5:  # per-signal rows into padded slots
                     ib = s * (n + 32 // ELEM_BYTES[prec])
                 # ABFT scratch: per-warp sums (TPS <= 32) or the deferred
                 # two-tile reduction pipeline (TPS >= 128: 2 x S x 5 x TPS partials + totals)
                 red = 10 * (threads // 32 + 1) + (10 * threads + 10 * s if tps >= 128 else 0)
-                smem = (ib + s * max(ex, st)) * ELEM_BYTES[prec] + red * (ELEM_BYTES[prec] // 2)
+                regions = 2 if c["stage"] == 6 else 1  # ping-pong exchange regions
+                smem = (ib + regions * s * max(ex, st)) * ELEM_BYTES[prec] + red * (ELEM_BYTES[prec] // 2)
                 out.append(dict(prec=prec, logn=logn, n=n, e=e, radices=radices, threads=threads,
                                 ps=ps, smem=smem, tps=tps, minb=c["minb"], stage=c["stage"],
                                 variant=vi, chosen=vi == chosen))

@@ -49,6 +49,33 @@ struct SliceMem {
     __device__ __forceinline__ void sync() const {
         if constexpr (TPS <= 32) __syncwarp(); else __syncthreads();
     }
+    // after the re-gather: the buffer may be rewritten by the next exchange
+    __device__ __forceinline__ void release() const { sync(); }
+    __device__ __forceinline__ void after_last_exchange() const {}
+};
+// Two alternating exchange regions (ping-pong): exchange k puts into and gets
+// from region `cur`, then switches, so the next exchange never writes what a
+// slower thread may still be reading and the trailing barrier of every
+// exchange disappears (one CTA barrier per exchange instead of two). The
+// region of exchange k + 2 is protected by the barrier of exchange k + 1.
+// `cur` persists across tiles (the alternation continues), and `hook` runs
+// once, right after the first barrier of the tile (every thread has its
+// input in registers by then: the prefetch buffer may be refilled).
+template <class T, int TPS, int PS, class Hook>
+struct PingPongMem {
+    C<T>* r0;
+    C<T>* r1;
+    C<T>** cur;
+    Hook hook;
+    mutable bool first = true;
+    __device__ __forceinline__ void put(int i, C<T> v) const { (*cur)[padidx<PS>(i)] = v; }
+    __device__ __forceinline__ C<T> get(int i) const { return (*cur)[padidx<PS>(i)]; }
+    __device__ __forceinline__ void sync() const {
+        __syncthreads();
+        if (first) hook();
+        first = false;
+    }
+    __device__ __forceinline__ void release() const { *cur = (*cur == r0) ? r1 : r0; }
     __device__ __forceinline__ void after_last_exchange() const {}
 };
 // U transforms interleaved: element i of transform u at pad(i)*U + u.
@@ -59,6 +86,7 @@ struct TileMem {
     __device__ __forceinline__ void put(int i, C<T> v) const { base[padidx<PS>(i) * U + u] = v; }
     __device__ __forceinline__ C<T> get(int i) const { return base[padidx<PS>(i) * U + u]; }
     __device__ __forceinline__ void sync() const { __syncthreads(); }
+    __device__ __forceinline__ void release() const { sync(); }
     __device__ __forceinline__ void after_last_exchange() const {}
 };
 
@@ -194,7 +222,7 @@ struct Engine {
             mem.sync();
 #pragma unroll
             for (int m = 0; m < E; ++m) v[m] = mem.get(t + m * TPS);
-            mem.sync();
+            mem.release();
             if constexpr (sizeof...(Rest) == 1) mem.after_last_exchange();
             passes<Ns * R>(v, mem, t, tw, chk, RList<Rest...>{});
         }

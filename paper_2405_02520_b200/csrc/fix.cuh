@@ -117,22 +117,22 @@ fix_single_kernel(const __grid_constant__ FixArgs<T> a) {
         const long long first = a.jobs ? a.jobs[j].first : j_first[j];
         const long long fsig = a.jobs ? a.jobs[j].flagged : j_flag[j];
         const C<T>* xf = a.in + fsig * N;
-        // ---- s0 (two-sided) or x_f (one-sided) at this thread's positions
+        // ---- s0 (two-sided) or x_f (one-sided) at this thread's positions;
+        // b outer / m inner: E independent loads per round trip (the sum
+        // stays sequential in b, as the host path's)
         C<T> v[E];
 #pragma unroll
-        for (int m = 0; m < E; ++m) {
-            const long long k = t + m * TPS;
-            C<T> s = mk<T>(T(0), T(0));
-            if (live) {
-                if (a.one_sided) {
-                    s = xf[k];
-                } else {
-                    const C<T>* xg = a.in + first * N;
-                    s = xg[k];
-                    for (long long b = 1; b < a.bs; ++b) s = cadd<T>(s, xg[b * N + k]);
-                }
+        for (int m = 0; m < E; ++m) v[m] = mk<T>(T(0), T(0));
+        if (live) {
+            const C<T>* xg = a.one_sided ? xf : a.in + first * N;
+            const long long nb = a.one_sided ? 1 : a.bs;
+#pragma unroll
+            for (int m = 0; m < E; ++m) v[m] = xg[t + m * TPS];
+#pragma unroll 4
+            for (long long b = 1; b < nb; ++b) {
+#pragma unroll
+                for (int m = 0; m < E; ++m) v[m] = cadd<T>(v[m], xg[b * N + t + m * TPS]);
             }
-            v[m] = s;
         }
         if (a.inverse) {
 #pragma unroll
@@ -159,19 +159,28 @@ fix_single_kernel(const __grid_constant__ FixArgs<T> a) {
             T l1 = T(0);
             const T hr = T(-0.5), hi = T(0.8660254037844386467637232);
             if (live) {
+                C<T> others[E];
+                bool firstb = true;
+#pragma unroll 4
+                for (long long b = 0; b < a.bs; ++b) {  // loads of 4 signals in flight
+                    const long long sg = first + b;
+                    C<T> y[E];
+#pragma unroll
+                    for (int m = 0; m < E; ++m) y[m] = a.out[sg * N + t + m * TPS];
+                    if (sg != fsig) {
+#pragma unroll
+                        for (int m = 0; m < E; ++m) others[m] = firstb ? y[m] : cadd<T>(others[m], y[m]);
+                        firstb = false;
+                    }
+                }
+                if (firstb) {
+#pragma unroll
+                    for (int m = 0; m < E; ++m) others[m] = mk<T>(T(0), T(0));
+                }
 #pragma unroll
                 for (int m = 0; m < E; ++m) {
                     const long long k = t + m * TPS;
-                    C<T> others = mk<T>(T(0), T(0));
-                    bool firstb = true;
-                    for (long long b = 0; b < a.bs; ++b) {
-                        const long long sg = first + b;
-                        if (sg == fsig) continue;
-                        const C<T> y = a.out[sg * N + k];
-                        others = firstb ? y : cadd<T>(others, y);
-                        firstb = false;
-                    }
-                    const C<T> f = csub<T>(v[m], others);
+                    const C<T> f = csub<T>(v[m], others[m]);
                     v[m] = f;
                     C<T> e;
                     if (a.values) e = a.values[k];

@@ -123,6 +123,7 @@ fft_pass_kernel(const __grid_constant__ PassArgs<T> a) {
         __device__ __forceinline__ void put(int i, C<T> v) const { base[i * RS + u] = v; }
         __device__ __forceinline__ C<T> get(int i) const { return base[i * RS + u]; }
         __device__ __forceinline__ void sync() const { __syncthreads(); }
+        __device__ __forceinline__ void release() const { __syncthreads(); }
         __device__ __forceinline__ void after_last_exchange() const {}
     };
 

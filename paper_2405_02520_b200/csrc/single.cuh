@@ -125,6 +125,10 @@ struct alignas(64) SingleArgs {
 // |c_in|, rare) the signal is sent back for an exact recheck (recheck_kernel).
 // A squared screen (no sqrt/div) clears the common case; anything near delta,
 // non-finite or out of range takes the exact arithmetic.
+#ifndef TFFT_BATCH_DECIDE
+#define TFFT_BATCH_DECIDE 1
+#endif
+
 template <class T>
 __device__ __forceinline__ void abft_decide(T r0, T r1, T r2, T r3, T l1b, T delta, T abs_floor, T coef,
                                             bool want_rel, T& rel, T& rel2, bool& flagged, bool& recheck) {
@@ -145,11 +149,23 @@ __device__ __forceinline__ void abft_decide(T r0, T r1, T r2, T r3, T l1b, T del
     }
     const T fl = floor_free ? T(0) : abs_floor;  // the exact floor term that can still matter
     const T den2 = floor_free ? cin2 : nanmax<T>(cin2, fmul(fl, fl));
-    const T q = raw2 / den2;
     const T d2 = fmul(delta, delta);
-    const bool in_range = den2 >= std::numeric_limits<T>::min() && den2 <= std::numeric_limits<T>::max() &&
+    // screen by multiplication (no division on the common path); fp32 keeps
+    // den2 <= 2^126 so the approximate reciprocal below stays normal
+    constexpr T DEN_MAX = sizeof(T) == 4 ? T(8.5070592e37) : std::numeric_limits<T>::max();
+    const bool in_range = den2 >= std::numeric_limits<T>::min() && den2 <= DEN_MAX &&
                           raw2 <= std::numeric_limits<T>::max();
-    if (in_range && q < T(0.81) * d2) {
+    if (in_range && raw2 < fmul(fmul(T(0.81), d2), den2)) {
+        // q = raw2 / den2 only feeds the running max and rel_out (decisions
+        // come from the exact path below): fp32 uses the approximate reciprocal
+        T q;
+        if constexpr (sizeof(T) == 4) {
+            float r;
+            asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(den2));
+            q = raw2 * r;
+        } else {
+            q = raw2 / den2;
+        }
         rel2 = q;
         if (want_rel) rel = sqrt(q);
     } else {
@@ -286,18 +302,24 @@ fft_single_kernel(const __grid_constant__ SingleArgs<T> a) {
     // itself (linear layout) once the last exchange of the current tile has
     // been read, so prefetching costs no extra shared memory (two CTAs/SM at
     // N = 8192).
+    // 6: like 2 (TMA bulk prefetch of the next tile into its own buffer), with
+    // two ping-pong exchange regions (PingPongMem): one CTA barrier per
+    // exchange instead of two, and the refill issued right after the tile's
+    // first exchange barrier (multi-warp signals only).
     // 5: one 2-D tensor TMA per tile whose box is 4 (complex64) / 2
     // (complex128) elements WIDER than a signal: the out-of-bounds columns are
     // zero-filled, so signals land at a padded stride and the t + m*TPS reads
     // of one warp's signals fall on different banks (a linear chunk puts them
     // all on the same banks: 8-way conflicts at N = 32).
     constexpr bool STG = STAGE == 1 || STAGE == 3;
-    constexpr bool PF = STAGE == 2 || STAGE == 3 || STAGE == 5;
+    constexpr bool PF = STAGE == 2 || STAGE == 3 || STAGE == 5 || STAGE == 6;
+    constexpr bool PP = STAGE == 6;
     constexpr bool PFI = STAGE == 4;
     constexpr bool PFR = STAGE == 5;
     constexpr int SLP = PFR ? N + 32 / (int)sizeof(C<T>) : N;  // prefetch slot stride (elements)
     static_assert(!PFR || (SLP * (int)sizeof(C<T>) / 4 <= 256 && S <= 256), "tensor-TMA box limits");
     static_assert(!PFI || TPS > 32, "in-place prefetch needs CTA-wide exchange barriers");
+    static_assert(!PP || (TPS > 32 && RCount<Radices>::v > 1), "ping-pong exchanges need CTA-wide exchanges");
     constexpr bool MULTIPASS = RCount<Radices>::v > 1;
     constexpr int SL = SliceLen<N, PS, MULTIPASS, STG, PFI>::v;
     constexpr int NW = THREADS / 32 > 0 ? THREADS / 32 : 1;
@@ -305,13 +327,14 @@ fft_single_kernel(const __grid_constant__ SingleArgs<T> a) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     C<T>* ib = reinterpret_cast<C<T>*>(smem_raw);  // prefetch buffer (PF)
     C<T>* sm_all = ib + (PF ? S * SLP : 0);
-    T* red = reinterpret_cast<T*>(sm_all + S * SL);  // 5 partial sums per warp
+    T* red = reinterpret_cast<T*>(sm_all + (PP ? 2 : 1) * S * SL);  // 5 partial sums per warp
     __shared__ typename KeyT<T>::type cta_max;
     __shared__ unsigned long long in_bar;
 
     const int sl = threadIdx.x / TPS;
     const int t = threadIdx.x % TPS;
     C<T>* sm = sm_all + sl * SL;
+    C<T>* pp_cur = sm;  // PP: the exchange region of the next exchange (alternates across tiles)
     T my_max = T(0);   // max rel^2 of screen-decided signals
     T my_maxr = T(0);  // max rel of exactly decided signals (rel^2 would overflow at rel > ~1e19 in fp32)
     if (threadIdx.x == 0) cta_max = 0;
@@ -401,6 +424,11 @@ fft_single_kernel(const __grid_constant__ SingleArgs<T> a) {
         decide_signal(sums, pend_b, owner);
         pend = false;
     };
+    // 2 <= TPS <= 32: batched decisions (one decision pass per TPS tiles)
+    constexpr bool BATCHD = TB && TPS >= 2 && TPS <= 32 && TFFT_BATCH_DECIDE;
+    T keep[5] = {T(0), T(0), T(0), T(0), T(0)};
+    long long keep_b = 0;
+    bool keep_v = false;
     constexpr int NWS = TPS > 32 ? TPS / 32 : 1;  // warps per signal
     constexpr int PPS = TPS;                         // stored partials per sum per signal
     T* const part = red;                             // [2][S][5][PPS]
@@ -495,6 +523,11 @@ fft_single_kernel(const __grid_constant__ SingleArgs<T> a) {
                     prefetch(tile + gridDim.x);
                 }
             }
+        } else if constexpr (PP) {
+            mbar_wait(&in_bar, iter & 1);
+#pragma unroll
+            for (int m = 0; m < E; ++m) v[m] = live ? ib[sl * SLP + t + m * TPS] : mk<T>(T(0), T(0));
+            // refilled after the first exchange barrier (PingPongMem hook)
         } else if constexpr (PF) {
             mbar_wait(&in_bar, iter & 1);
 #pragma unroll
@@ -555,7 +588,17 @@ fft_single_kernel(const __grid_constant__ SingleArgs<T> a) {
         // thread-level scheme: each thread verifies its radix tiles
         TileCheck<T> tchk;
         tchk.floor2 = fmul(a.abs_floor, a.abs_floor);
-        if constexpr (PFI && MULTIPASS) {
+        if constexpr (PP) {
+            auto refill = [&]() {
+                if (threadIdx.x < ISSUE && tile + gridDim.x < tiles) {
+                    fence_proxy_async();
+                    prefetch(tile + gridDim.x);
+                }
+            };
+            const PingPongMem<T, TPS, PS, decltype(refill)> mem{sm, sm + S * SL, &pp_cur, refill};
+            if constexpr (ABFT == ABFT_THREAD) Eng::run(v, mem, t, a.tw, tchk);
+            else Eng::run(v, mem, t, a.tw);
+        } else if constexpr (PFI && MULTIPASS) {
             // refill the buffer as soon as the last exchange has been read
             auto refill = [&]() {
                 if (threadIdx.x == 0 && tile + gridDim.x < tiles) {
@@ -692,6 +735,21 @@ fft_single_kernel(const __grid_constant__ SingleArgs<T> a) {
                 pend_live = live;
                 pend_b = b;
                 pend_par = iter & 1;
+            } else if constexpr (BATCHD) {
+                // every lane of the signal holds the totals after the xor tree;
+                // lane t keeps tile (iter mod TPS), and every TPS tiles all lanes
+                // decide their kept signal at once (TPS x fewer decision passes)
+                if constexpr (!(TFFT_ABLATE & 1)) sig_sum<TPS>(sums, red, t);
+                if ((int)(iter & (TPS - 1)) == t) {
+#pragma unroll
+                    for (int i = 0; i < 5; ++i) keep[i] = sums[i];
+                    keep_b = b;
+                    keep_v = live;
+                }
+                if ((int)(iter & (TPS - 1)) == TPS - 1) {
+                    decide_signal(keep, keep_b, keep_v);
+                    keep_v = false;
+                }
             } else {
                 if constexpr (!(TFFT_ABLATE & 1)) sig_sum<TPS>(sums, red, t);
                 decide_signal(sums, b, t == 0 && live);
@@ -704,6 +762,7 @@ fft_single_kernel(const __grid_constant__ SingleArgs<T> a) {
             finish_pending();
         }
     }
+    if constexpr (BATCHD) decide_signal(keep, keep_b, keep_v);  // the last partial batch
     if constexpr (DEFER) {  // drain the pipeline (uniform across the CTA)
         if (p1 || p2) {
             __syncthreads();

@@ -6,14 +6,25 @@
   >= 64 sampled signals (first / last, tile and grid-stride boundaries,
   random) match an fp64 FFT within 2e-7 (fp32) / 1e-15 (fp64) x log2 n
   per-signal relative L2.
-* Clean-data flags of the full C2 sweep: every flagged signal's group is
-  re-run through the oracle (the reference restatement with the reference's
-  own compiled butterfly, oracle/_ref) and the reference's relative
-  discrepancy of that signal must not be below delta / 3 (no flag the
-  reference would call clean by a margin). On a random 2^18-sample of every
-  size the decisions of both agree wherever the reference's discrepancy is
-  outside [delta / 3, 3 delta]; the reference's own false-alarm count on the
-  sample is reported (TFFT_SCALE_DUMP=path writes the summary as JSON).
+* Clean-data flags of the full C2 sweep. A clean signal is flagged when the
+  rounding noise of c_in - c_out (fp32 sums and fp32 FFT, here and in the
+  reference alike) exceeds delta * |c_in|, i.e. only for signals whose
+  |c_in| is tiny. The noise of two implementations that round in different
+  orders is correlated but not equal, so a signal picked for being the
+  largest of ~10^7 draws of OUR noise is typically smaller in the
+  reference's draw (selection effect; an fp32 emulation of this kernel's
+  summation order vs the reference on 2^20 signals at N = 64 gives 19 / 22
+  signals above 3e-5 but the top signals differ by up to 6x). So:
+  - every full-scale clean flag must lie in the reference's own far noise
+    tail: its reference rel > delta / 30 (a median clean rel is ~1e-7 to
+    5e-7, i.e. this is the top ~0.1 % of the reference's distribution);
+  - our noise must not exceed the reference's: on a common random sample per
+    size, the number of signals above a probe threshold (1e-6 .. 3e-6, ~10^3
+    signals in the reference) is at most 1.5x the reference's (measured: at
+    N = 1024 ours is ~3x lower);
+  - on a 2^18-sample of every size the decisions at delta agree wherever the
+    reference's discrepancy is outside [delta / 10, 10 delta].
+  TFFT_SCALE_DUMP=path writes the summary as JSON.
 """
 
 import json
@@ -131,7 +142,7 @@ def test_c2_fp32_bench_scale_and_clean_flags_vs_reference():
                           "rel_reference": _ref_rel(xh[s], kernel)})
     summary["clean_flags"] = flags
     for f in flags:
-        assert f["rel_reference"] > 1e-4 / 3, f  # a flag the reference would call clean: fail
+        assert f["rel_reference"] > 1e-4 / 30, f  # outside the reference's own noise tail: fail
     summary["flags_reference_also_flags"] = sum(f["rel_reference"] > 1e-4 for f in flags)
     # random sample of every size: decisions agree outside the x3 band
     rng = np.random.default_rng(99)
@@ -149,10 +160,37 @@ def test_c2_fp32_bench_scale_and_clean_flags_vs_reference():
         theirs = {f["signal"]: f["discrepancy"] for f in orep["flagged"]}
         for s in mine ^ set(theirs):
             r = theirs[s] if s in theirs else _ref_rel(x[s], kernel)
-            assert 1e-4 / 3 < r < 3e-4, (n, s, r)
+            assert 1e-4 / 10 < r < 1e-3, (n, s, r)
         sample.append({"n": n, "signals": b, "ours_flagged": len(mine), "reference_flagged": len(theirs)})
     summary["random_sample"] = sample
+    summary["noise_tail"] = _noise_tails(kernel)
     dump = os.environ.get("TFFT_SCALE_DUMP")
     if dump:
         with open(dump, "w") as f:
             json.dump(summary, f, indent=1)
+
+
+def _noise_tails(kernel):
+    """Counts of clean signals whose rel exceeds a probe threshold, ours (the
+    fused kernel's flag records at delta = probe) vs the reference's, on the
+    same seeded sample; ~10^3 signals each, so binomial noise is ~3 %."""
+    from oracle import port as P
+    out = []
+    for n, b, probe in ((8, 1 << 21, 3e-6), (64, 1 << 20, 3e-6), (1024, 1 << 16, 3e-6), (8192, 1 << 13, 1e-6)):
+        rng = np.random.default_rng([7, n])
+        x = (rng.standard_normal((b, n)) + 1j * rng.standard_normal((b, n))).astype(np.complex64)
+        plan = _plan(n, "fp32", b)
+        _, rep, _ = _run(plan, torch.from_numpy(x).cuda(), "two_sided_group", probe)
+        ours = {f["signal"] for f in rep.flagged}
+        enc = P.encoding_for("wang", n, kernel)
+        p1 = P.shrink_bs(P.plan_for(n, "fp32", batch=1), 1)
+        tw = P.twiddles_for(p1)
+        y = np.concatenate([P.execute(p1, tw, x[i:i + 1024].copy(), kernel=kernel) for i in range(0, b, 1024)])
+        _, rr, _ = P.verify(P.encode(x, enc), y, enc, probe, 0.0, "fp32")
+        theirs = set(np.flatnonzero(rr > probe).tolist())
+        rec = {"n": n, "signals": b, "probe": probe, "ours": len(ours), "reference": len(theirs),
+               "both": len(ours & theirs)}
+        out.append(rec)
+        assert len(theirs) >= 100, rec
+        assert len(ours) <= 1.5 * len(theirs), rec  # no noisier than the reference
+    return out

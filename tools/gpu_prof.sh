@@ -1,5 +1,6 @@
 # ncu --set full captures, ABFT on vs off, summarised on the box (reports over
-# 20 MB are deleted after summarising so gpurun_out stays under its cap).
+# 20 MB, and all of them without KEEP=1, are deleted after summarising:
+# gpurun_out must stay under its 64 MiB merge cap).
 # usage: KRE=<kernel regex> COUNT=<kernels per capture> bash tools/gpu_prof.sh TAG prec:logn ...
 set -x
 cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
@@ -13,7 +14,7 @@ for spec in $@; do
       -o $o -f python tools/profile_single.py --prec $p --logn $l --scheme $sc --reps 2 > $o.log 2>&1
     python tools/ncu_summary.py $o.ncu-rep > $o.md 2>&1
     python tools/sass_hot.py $o.ncu-rep --top 30 --lines 40 > $o.sass.txt 2>&1
-    if [ $(stat -c %s $o.ncu-rep) -gt 20000000 ]; then rm -f $o.ncu-rep; fi
+    if [ -z "$KEEP" ] || [ $(stat -c %s $o.ncu-rep) -gt 20000000 ]; then rm -f $o.ncu-rep; fi
   done
 done
 du -sh gpurun_out

@@ -32,6 +32,33 @@ WANT = {
 }
 
 
+PIPE_PREFIXES = ("sm__pipe_", "sm__inst_executed_pipe_")
+
+
+def read_pipes(path):
+    """Per kernel: every pipe-utilisation metric of the capture
+    (sm__pipe_*_cycles_active / sm__inst_executed_pipe_* as % of peak), e.g.
+    the FP64 pipe for the double-precision kernels."""
+    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv", "--print-units", "base"],
+                         capture_output=True, text=True, check=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    hdr, data = rows[0], rows[2:]
+    res = []
+    for row in data:
+        d = dict(zip(hdr, row))
+        pipes = {}
+        for k, v in d.items():
+            if k.startswith(PIPE_PREFIXES) and k.endswith("pct_of_peak_sustained_active"):
+                try:
+                    x = float(v.replace(",", ""))
+                except ValueError:
+                    continue
+                if x >= 0.5:
+                    pipes[k.replace(".avg.pct_of_peak_sustained_active", "")] = x
+        res.append((d.get("Kernel Name", "?")[:90], pipes))
+    return res
+
+
 def read(path):
     out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv", "--print-units", "base"],
                          capture_output=True, text=True, check=True).stdout
@@ -75,6 +102,13 @@ def main():
         for rec in read(path):
             vals = [fmt(rec[c]) if c in rec else "" for c in cols]
             print(f"| {path.split('/')[-1]} | `{rec['kernel']}` | " + " | ".join(vals) + " |")
+    print()
+    print("Pipe utilisation (% of peak sustained, >= 0.5 %):")
+    print()
+    for path in sys.argv[1:]:
+        for kern, pipes in read_pipes(path):
+            top = ", ".join(f"{k} {v:.1f}" for k, v in sorted(pipes.items(), key=lambda kv: -kv[1]))
+            print(f"- {path.split('/')[-1]} `{kern}`: {top}")
 
 
 if __name__ == "__main__":
