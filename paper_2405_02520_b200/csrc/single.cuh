@@ -470,7 +470,8 @@ fft_single_kernel(const __grid_constant__ SingleArgs<T> a) {
     // The e^T W row (<= 16 KB, signals of >= 2 warps) staged in shared memory once per CTA: the
     // per-tile reads are then LDS instead of L1-hit LDGs (fp32 N = 2048:
     // 0.512 -> 0.491 ms; at 32 KB the lost occupancy costs more than it saves)
-    constexpr bool EWS = TFFT_EW_SMEM && TB && TPS >= 64 && N * (int)sizeof(C<T>) <= 16384;
+    // (not with the ping-pong regions, whose dynamic smem already sets the occupancy)
+    constexpr bool EWS = TFFT_EW_SMEM && TB && TPS >= 64 && N * (int)sizeof(C<T>) <= 16384 && !PP;
     __shared__ C<T> etw_sm[EWS ? N : 1];
     if constexpr (EWS) {
         for (int i = threadIdx.x; i < N; i += THREADS) etw_sm[i] = a.etw[i];
