@@ -291,13 +291,25 @@ fft_pass_kernel(const __grid_constant__ PassArgs<T> a) {
         }
 
         if constexpr (KIND == KIND_FIRST && ABFT != ABFT_OFF) {
-            C<T> cin = mk<T>(T(0), T(0));
-            C<T> l1p = mk<T>(T(0), T(0));  // l1 upper bound sum(|re| + |im|), see abft_decide
+            // KA independent partial sums (short chains), combined pairwise
+            constexpr int KA = E >= 16 ? 4 : (E >= 4 ? 2 : 1);
+            C<T> ca[KA], la[KA];  // la: l1 upper bound sum(|re| + |im|), see abft_decide
+#pragma unroll
+            for (int k = 0; k < KA; ++k) ca[k] = la[k] = mk<T>(T(0), T(0));
 #pragma unroll
             for (int m = 0; m < E; ++m) {
-                cin = cmac<T>(cin, v[m], ew[m]);
-                l1p = cadd<T>(l1p, cabs2<T>(v[m]));
+                ca[m % KA] = cmac<T>(ca[m % KA], v[m], ew[m]);
+                la[m % KA] = cadd<T>(la[m % KA], cabs2<T>(v[m]));
             }
+#pragma unroll
+            for (int w = KA / 2; w >= 1; w /= 2) {
+#pragma unroll
+                for (int k = 0; k < w; ++k) {
+                    ca[k] = cadd<T>(ca[k], ca[k + w]);
+                    la[k] = cadd<T>(la[k], la[k + w]);
+                }
+            }
+            const C<T> cin = ca[0], l1p = la[0];
             T s[3] = {cin.x, cin.y, fadd(l1p.x, l1p.y)};
             warp_partials<3>(s, red);  // summed by thread 0 after the tile's trailing barrier
         }

@@ -556,15 +556,32 @@ fft_single_kernel(const __grid_constant__ SingleArgs<T> a) {
         }
 
         // ---- left-side input checksum on the pristine values
+        // KA independent partial sums per quantity (short dependency chains
+        // the scheduler can interleave with the first radix pass), combined
+        // pairwise in a fixed order
+        constexpr int KA = E >= 16 ? 4 : (E >= 4 ? 2 : 1);
         C<T> cin = mk<T>(T(0), T(0));
         C<T> l1p = mk<T>(T(0), T(0));  // (sum |re|, sum |im|): the l1 upper bound
         if constexpr (TB) {
+            C<T> ca[KA], la[KA];
+#pragma unroll
+            for (int k = 0; k < KA; ++k) ca[k] = la[k] = mk<T>(T(0), T(0));
 #pragma unroll
             for (int m = 0; m < E; ++m) {
                 if constexpr (!TFFT_EW_HOIST) ew[m] = EWS ? etw_sm[t + m * TPS] : __ldg(a.etw + t + m * TPS);
-                if constexpr (!(TFFT_ABLATE & 2)) cin = cmac<T>(cin, v[m], ew[m]);
-                if constexpr (!(TFFT_ABLATE & 4)) l1p = cadd<T>(l1p, cabs2<T>(v[m]));
+                if constexpr (!(TFFT_ABLATE & 2)) ca[m % KA] = cmac<T>(ca[m % KA], v[m], ew[m]);
+                if constexpr (!(TFFT_ABLATE & 4)) la[m % KA] = cadd<T>(la[m % KA], cabs2<T>(v[m]));
             }
+#pragma unroll
+            for (int w = KA / 2; w >= 1; w /= 2) {
+#pragma unroll
+                for (int k = 0; k < w; ++k) {
+                    ca[k] = cadd<T>(ca[k], ca[k + w]);
+                    la[k] = cadd<T>(la[k], la[k + w]);
+                }
+            }
+            cin = ca[0];
+            l1p = la[0];
         }
         int fw = a.f_where, fc = a.f_comp, fb = a.f_bit;
         long long fs = a.f_signal, fe = a.f_elem;
@@ -699,10 +716,18 @@ fft_single_kernel(const __grid_constant__ SingleArgs<T> a) {
             C<T> cout = mk<T>(T(0), T(0));
             if constexpr (ABFT == ABFT_WANG) {
                 // e_k = w3^(k mod 3): sum per residue class, then 3 weights.
-                C<T> acc[3] = {mk<T>(T(0), T(0)), mk<T>(T(0), T(0)), mk<T>(T(0), T(0))};
+                // six partial sums for long rows (m mod 6 keeps the class m mod 3)
+                constexpr int K6 = E >= 16 ? 6 : 3;
+                C<T> acc[K6];
+#pragma unroll
+                for (int k = 0; k < K6; ++k) acc[k] = mk<T>(T(0), T(0));
 #pragma unroll
                 for (int m = 0; m < E; ++m)
-                    if constexpr (!(TFFT_ABLATE & 8)) acc[m % 3] = cadd<T>(acc[m % 3], v[m]);
+                    if constexpr (!(TFFT_ABLATE & 8)) acc[m % K6] = cadd<T>(acc[m % K6], v[m]);
+                if constexpr (K6 == 6) {
+#pragma unroll
+                    for (int k = 0; k < 3; ++k) acc[k] = cadd<T>(acc[k], acc[k + 3]);
+                }
                 constexpr int tau = TPS % 3;  // 1 or 2 (TPS is a power of two)
                 const int t0 = t % 3;
                 constexpr T hr = T(-0.5), hi = T(0.8660254037844386467637232);

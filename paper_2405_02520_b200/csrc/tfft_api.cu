@@ -227,6 +227,12 @@ struct tfft_plan {
     void* d_rel = nullptr;          // campaign per-signal rel discrepancies
     size_t rel_bytes = 0;
     cudaEvent_t ev_done = nullptr;  // detection summary landed in h_cnt
+    // device-side correction off the caller's stream: the fix pass (latency
+    // bound, ~10-50 us when something was flagged) overlaps whatever the
+    // caller queues next; _finish orders the caller's stream behind it
+    cudaStream_t s_fix = nullptr;
+    cudaEvent_t ev_kern = nullptr;
+    bool fix_side = false;
     // host-streaming path (tfft_run_protected_host): a ring of device chunk
     // buffers, copy streams for each direction, per-slot events
     static constexpr int kRing = 3;
@@ -746,6 +752,8 @@ int tfft_plan_destroy(tfft_plan* p) {
     cudaFree(p->d_ftab);
     cudaFree(p->d_rel);
     if (p->ev_done) cudaEventDestroy(p->ev_done);
+    if (p->ev_kern) cudaEventDestroy(p->ev_kern);
+    if (p->s_fix) cudaStreamDestroy(p->s_fix);
     cudaFree(p->ring);
     if (p->h_stage) cudaFreeHost(p->h_stage);
     for (int i = 0; i < tfft_plan::kRing; ++i) {
@@ -906,14 +914,24 @@ int tfft_protect_launch(tfft_plan* p, const void* in, void* out, int64_t batch, 
     if (rc) return rc;
     if (!prot) return TFFT_OK;
     // single-kernel sizes: the corrections run on the device right behind the
-    // transform (fix.cuh), so the summary below already carries the verdicts
+    // transform (fix.cuh), so the summary below already carries the verdicts.
+    // The fix pass and the summary copy go to the plan's side stream (after
+    // the transform): the caller's stream moves on to its next work at once.
+    p->fix_side = false;
+    cudaStream_t sum_st = st;
     if (p->single && p->dev_fix && scheme != TFFT_SCHEME_NONE) {
+        if (!p->s_fix) CU(cudaStreamCreateWithFlags(&p->s_fix, cudaStreamNonBlocking));
+        if (!p->ev_kern) CU(cudaEventCreateWithFlags(&p->ev_kern, cudaEventDisableTiming));
+        CU(cudaEventRecord(p->ev_kern, st));
+        CU(cudaStreamWaitEvent(p->s_fix, p->ev_kern, 0));
         rc = launch_fix(p, in, out, etw, values, delta, abs_floor, inverse ? 1 : 0,
-                        scheme == TFFT_SCHEME_ONE_SIDED, nullptr, 0, st);
+                        scheme == TFFT_SCHEME_ONE_SIDED, nullptr, 0, p->s_fix);
         if (rc && rc != TFFT_EUNSUPPORTED) return rc;
+        sum_st = p->s_fix;
+        p->fix_side = true;
     }
     // the (tiny) detection summary rides back behind the transform
-    rc = enqueue_summary(p, st);
+    rc = enqueue_summary(p, sum_st);
     if (rc) return rc;
     return TFFT_OK;
 }
@@ -1230,6 +1248,10 @@ int tfft_protect_finish(tfft_plan* p, const void* in, void* out, int64_t batch, 
     RecheckFn resolve = [&](const std::vector<long long>& sg, std::vector<double>& rr) {
         return recheck_device(p, in, out, sg, etw, values, abs_floor, rr, st);
     };
+    if (p->fix_side) {  // later work on the caller's stream sees the corrected outputs
+        CU(cudaStreamWaitEvent(st, p->ev_done, 0));
+        p->fix_side = false;
+    }
     rc = read_summary(p, batch, st, rep, flags, delta, resolve);  // waits for the summary copy
     if (rc) return rc;
     const FixHead fh = p->h_cnt->fix;

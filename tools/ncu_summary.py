@@ -48,7 +48,8 @@ def read_pipes(path):
         d = dict(zip(hdr, row))
         pipes = {}
         for k, v in d.items():
-            if k.startswith(PIPE_PREFIXES) and k.endswith("pct_of_peak_sustained_active"):
+            if (k.startswith(PIPE_PREFIXES) and k.endswith("pct_of_peak_sustained_active")
+                    and not any(t in k for t in (".max.", ".min.", ".sum."))):
                 try:
                     x = float(v.replace(",", ""))
                 except ValueError:

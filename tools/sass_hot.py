@@ -30,7 +30,9 @@ def main():
     tot_i = tot_s = 0
     hot = []
     for r in rows:
-        if len(r) < len(hdr):
+        if r[:3] == hdr[:3]:
+            break  # the next kernel's section (captures with -c > 1): first kernel only
+        if len(r) < len(hdr) or not r[ix["Instructions Executed"]].strip().isdigit():
             continue
         src = r[ix["Source"]].strip()
         op = src.split()[0] if src else "?"
