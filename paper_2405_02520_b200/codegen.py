@@ -115,9 +115,10 @@ SINGLE_CANDIDATES = {
 # Round 2 (profiles/tune_r02_fp32.json, tune_r02_fp64.json; timed at a delta with no
 # clean-data false alarms): fp32 N = 32 -> 2 CTAs/SM, N = 1024 -> 3 CTAs/SM,
 # N = 8192 -> E = 32 in 256-thread CTAs (in-place TMA prefetch), fp64 N = 2048
-# -> ping-pong exchange regions (STAGE 6).
+# -> ping-pong exchange regions (STAGE 6); after the exchange-addressing
+# rewrite (profiles/tune_r02c_fp32.json) N = 64 -> TMA bulk prefetch (STAGE 2).
 SINGLE_CHOICE = {
-    "fp32": {1: 1, 2: 1, 3: 4, 4: 5, 5: 7, 6: 8, 7: 0, 8: 4, 9: 7, 10: 9, 11: 8, 12: 6, 13: 11},
+    "fp32": {1: 1, 2: 1, 3: 4, 4: 5, 5: 7, 6: 5, 7: 0, 8: 4, 9: 7, 10: 9, 11: 8, 12: 6, 13: 11},
     "fp64": {1: 1, 2: 2, 3: 3, 4: 7, 5: 5, 6: 4, 7: 0, 8: 4, 9: 6, 10: 4, 11: 8, 12: 4, 13: 2},
 }
 ELEM_BYTES = {"fp32": 8, "fp64": 16}

@@ -43,9 +43,12 @@ struct SmemLen { static constexpr int v = (PS == 0) ? L : L + (L >> PS) + 1; };
 // Signal-contiguous slice; signals never span warps when TPS <= 32.
 template <class T, int TPS, int PS>
 struct SliceMem {
+    static constexpr int kPS = PS;
     C<T>* base;
-    __device__ __forceinline__ void put(int i, C<T> v) const { base[padidx<PS>(i)] = v; }
-    __device__ __forceinline__ C<T> get(int i) const { return base[padidx<PS>(i)]; }
+    // p = padidx<PS>(i): the engine computes padded indices (mostly per-thread
+    // base + compile-time offset), the policy maps them to an address
+    __device__ __forceinline__ void putp(int p, C<T> v) const { base[p] = v; }
+    __device__ __forceinline__ C<T> getp(int p) const { return base[p]; }
     __device__ __forceinline__ void sync() const {
         if constexpr (TPS <= 32) __syncwarp(); else __syncthreads();
     }
@@ -68,8 +71,9 @@ struct PingPongMem {
     C<T>** cur;
     Hook hook;
     mutable bool first = true;
-    __device__ __forceinline__ void put(int i, C<T> v) const { (*cur)[padidx<PS>(i)] = v; }
-    __device__ __forceinline__ C<T> get(int i) const { return (*cur)[padidx<PS>(i)]; }
+    static constexpr int kPS = PS;
+    __device__ __forceinline__ void putp(int p, C<T> v) const { (*cur)[p] = v; }
+    __device__ __forceinline__ C<T> getp(int p) const { return (*cur)[p]; }
     __device__ __forceinline__ void sync() const {
         __syncthreads();
         if (first) hook();
@@ -81,10 +85,11 @@ struct PingPongMem {
 // U transforms interleaved: element i of transform u at pad(i)*U + u.
 template <class T, int U, int PS>
 struct TileMem {
+    static constexpr int kPS = PS;
     C<T>* base;
     int u;
-    __device__ __forceinline__ void put(int i, C<T> v) const { base[padidx<PS>(i) * U + u] = v; }
-    __device__ __forceinline__ C<T> get(int i) const { return base[padidx<PS>(i) * U + u]; }
+    __device__ __forceinline__ void putp(int p, C<T> v) const { base[p * U + u] = v; }
+    __device__ __forceinline__ C<T> getp(int p) const { return base[p * U + u]; }
     __device__ __forceinline__ void sync() const { __syncthreads(); }
     __device__ __forceinline__ void release() const { sync(); }
     __device__ __forceinline__ void after_last_exchange() const {}
@@ -212,16 +217,34 @@ struct Engine {
             for (int r = 0; r < R; ++r) v[q + r * SUB] = a[r];
         }
         if constexpr (sizeof...(Rest) > 0) {
+            // padded indices: one per-thread base and compile-time offsets
+            // whenever the stride is a multiple of the padding period (then
+            // pad(b + k) = pad(b) + pad(k) exactly), else per element
+            constexpr int PS = Mem::kPS;
+            constexpr bool PUT_LIN = PS == 0 || (Ns % (1 << PS)) == 0;
+            constexpr bool GET_LIN = PS == 0 || (TPS % (1 << PS)) == 0;
 #pragma unroll
             for (int q = 0; q < SUB; ++q) {
-                const int j = t + q * TPS;
-                const int base = (j / Ns) * Ns * R + (j & (Ns - 1));
+                const unsigned j = (unsigned)t + q * TPS;
+                const unsigned base = (j / Ns) * Ns * R + (j & (Ns - 1));
+                if constexpr (PUT_LIN) {
+                    const int pb = (int)(base + (PS ? base >> PS : 0u));
 #pragma unroll
-                for (int r = 0; r < R; ++r) mem.put(base + r * Ns, v[q + r * SUB]);
+                    for (int r = 0; r < R; ++r) mem.putp(pb + r * (Ns + (PS ? Ns >> PS : 0)), v[q + r * SUB]);
+                } else {
+#pragma unroll
+                    for (int r = 0; r < R; ++r) mem.putp(padidx<PS>((int)base + r * Ns), v[q + r * SUB]);
+                }
             }
             mem.sync();
+            if constexpr (GET_LIN) {
+                const int pt = (int)((unsigned)t + (PS ? (unsigned)t >> PS : 0u));
 #pragma unroll
-            for (int m = 0; m < E; ++m) v[m] = mem.get(t + m * TPS);
+                for (int m = 0; m < E; ++m) v[m] = mem.getp(pt + m * (TPS + (PS ? TPS >> PS : 0)));
+            } else {
+#pragma unroll
+                for (int m = 0; m < E; ++m) v[m] = mem.getp(padidx<PS>(t + m * TPS));
+            }
             mem.release();
             if constexpr (sizeof...(Rest) == 1) mem.after_last_exchange();
             passes<Ns * R>(v, mem, t, tw, chk, RList<Rest...>{});

@@ -82,6 +82,19 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
         : "memory");
 }
 
+// Engine memory policy of a pass tile: [L][U] rows of stride RS, lane u.
+template <class T, int RS>
+struct RowMem {
+    static constexpr int kPS = 0;
+    C<T>* base;
+    int u;
+    __device__ __forceinline__ void putp(int i, C<T> v) const { base[i * RS + u] = v; }
+    __device__ __forceinline__ C<T> getp(int i) const { return base[i * RS + u]; }
+    __device__ __forceinline__ void sync() const { __syncthreads(); }
+    __device__ __forceinline__ void release() const { __syncthreads(); }
+    __device__ __forceinline__ void after_last_exchange() const {}
+};
+
 template <class T, int L, int E, int U, int P, int KIND, int ABFT, int MINB, int PF, class Radices>
 __global__ void __launch_bounds__(U * (L / E), MINB)
 fft_pass_kernel(const __grid_constant__ PassArgs<T> a) {
@@ -117,15 +130,7 @@ fft_pass_kernel(const __grid_constant__ PassArgs<T> a) {
     const int t = threadIdx.x / U;
     const long long total = a.batch * a.tiles_per_sig;
 
-    struct Mem {
-        C<T>* base;
-        int u;
-        __device__ __forceinline__ void put(int i, C<T> v) const { base[i * RS + u] = v; }
-        __device__ __forceinline__ C<T> get(int i) const { return base[i * RS + u]; }
-        __device__ __forceinline__ void sync() const { __syncthreads(); }
-        __device__ __forceinline__ void release() const { __syncthreads(); }
-        __device__ __forceinline__ void after_last_exchange() const {}
-    };
+    using Mem = RowMem<T, RS>;
 
     // Tile order. The first pass with ABFT walks tile-position-major (all
     // signals' tile i, then tile i+1, ...) so concurrent CTAs read the same
@@ -207,6 +212,7 @@ fft_pass_kernel(const __grid_constant__ PassArgs<T> a) {
         cp_async_commit();
     }
 
+    const unsigned bbar_s = smem_u32(&bbar[0]);  // shared-window address, converted once
     unsigned it = 0;
     for (long long tix = blockIdx.x; tix < total; tix += gridDim.x, ++it) {
         C<T>* cur = (PF && (it & 1)) ? tile + BUFE : tile;
@@ -249,7 +255,7 @@ fft_pass_kernel(const __grid_constant__ PassArgs<T> a) {
             if (tix + gridDim.x < total)
                 issue_bulk(tix + gridDim.x, (it & 1) ? tile : tile + BUFE, (it & 1) ? etile : etile + ETWE,
                            &bbar[(it + 1) & 1]);
-            mbar_wait(&bbar[it & 1], (it >> 1) & 1);
+            mbar_wait_s(bbar_s + 8u * (it & 1), (it >> 1) & 1);
             if constexpr (KIND == KIND_LAST) {
 #pragma unroll
                 for (int m = 0; m < E; ++m) v[m] = cur[u * SU + t + m * TPS];

@@ -86,6 +86,12 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
         ::"r"(smem_u32(dst)), "l"(reinterpret_cast<unsigned long long>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
         : "memory");
 }
+__device__ __forceinline__ void tma_load_2d_s(unsigned dst, const CUtensorMap* map, int c0, int c1, unsigned bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+        ::"r"(dst), "l"(reinterpret_cast<unsigned long long>(map)), "r"(c0), "r"(c1), "r"(bar)
+        : "memory");
+}
 
 template <class T>
 struct alignas(64) SingleArgs {
@@ -341,16 +347,17 @@ fft_single_kernel(const __grid_constant__ SingleArgs<T> a) {
 
     const long long tiles = (a.batch + S - 1) / S;
     C<T>* const pf_dst = PFI ? sm_all : ib;
+    const unsigned pf_dst_s = smem_u32(pf_dst), in_bar_s = smem_u32(&in_bar);  // once, outside the tile loop
     auto prefetch = [&](long long tl) {  // thread 0 only (PFR: threads 0..S-1, one row each)
         const long long nsig = (a.batch - tl * S) < S ? (a.batch - tl * S) : S;
         if constexpr (PFR) {  // the full box arrives, OOB rows / columns as zeros
             (void)nsig;
-            mbar_expect_tx(&in_bar, (unsigned)(S * SLP * sizeof(C<T>)));
-            tma_load_2d(pf_dst, &a.tmap, 0, (int)(tl * S), &in_bar);
+            mbar_expect_tx_s(in_bar_s, (unsigned)(S * SLP * sizeof(C<T>)));
+            tma_load_2d_s(pf_dst_s, &a.tmap, 0, (int)(tl * S), in_bar_s);
         } else {
             const unsigned bytes = (unsigned)(nsig * N * sizeof(C<T>));
-            mbar_expect_tx(&in_bar, bytes);
-            bulk_g2s(pf_dst, a.in + tl * S * N, bytes, &in_bar);
+            mbar_expect_tx_s(in_bar_s, bytes);
+            bulk_g2s_s(pf_dst_s, a.in + tl * S * N, bytes, in_bar_s);
         }
     };
     constexpr int ISSUE = 1;  // the thread that issues (and arrives on) each prefetch
@@ -494,7 +501,7 @@ fft_single_kernel(const __grid_constant__ SingleArgs<T> a) {
         }
         C<T> v[E];
         if constexpr (PF && STG) {
-            mbar_wait(&in_bar, iter & 1);
+            mbar_wait_s(in_bar_s, iter & 1);
             // contiguous chunk -> padded slices (16-byte reads, 8-byte writes)
             for (int e = threadIdx.x * (16 / (int)sizeof(C<T>)); e < S * N; e += THREADS * (16 / (int)sizeof(C<T>))) {
                 if constexpr (sizeof(T) == 4) {
@@ -514,7 +521,7 @@ fft_single_kernel(const __grid_constant__ SingleArgs<T> a) {
             for (int m = 0; m < E; ++m) v[m] = live ? sm[t + m * TPS] : mk<T>(T(0), T(0));
             __syncthreads();
         } else if constexpr (PFI) {
-            mbar_wait(&in_bar, iter & 1);
+            mbar_wait_s(in_bar_s, iter & 1);
 #pragma unroll
             for (int m = 0; m < E; ++m) v[m] = live ? sm_all[sl * N + t + m * TPS] : mk<T>(T(0), T(0));
             __syncthreads();  // linear tile consumed; the exchanges below reuse the buffer
@@ -525,12 +532,12 @@ fft_single_kernel(const __grid_constant__ SingleArgs<T> a) {
                 }
             }
         } else if constexpr (PP) {
-            mbar_wait(&in_bar, iter & 1);
+            mbar_wait_s(in_bar_s, iter & 1);
 #pragma unroll
             for (int m = 0; m < E; ++m) v[m] = live ? ib[sl * SLP + t + m * TPS] : mk<T>(T(0), T(0));
             // refilled after the first exchange barrier (PingPongMem hook)
         } else if constexpr (PF) {
-            mbar_wait(&in_bar, iter & 1);
+            mbar_wait_s(in_bar_s, iter & 1);
 #pragma unroll
             for (int m = 0; m < E; ++m) v[m] = live ? ib[sl * SLP + t + m * TPS] : mk<T>(T(0), T(0));
             __syncthreads();  // everyone has the tile in registers: refill the buffer
