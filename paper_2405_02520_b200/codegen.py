@@ -40,10 +40,16 @@ SINGLE_CANDIDATES = {
         5: _cands((8, (8, 4), 256, 1, 1), (8, (8, 4), 256, 1, 0), (16, (16, 2), 256, 1, 1),
                   (32, (32,), 256, 1, 1), (8, (8, 4), 256, 1, 3), (8, (8, 4), 256, 1, 2),
                   (8, (8, 4), 256, 1, 5), (8, (8, 4), 256, 2, 5), (16, (16, 2), 256, 1, 5),
-                  (4, (4, 4, 2), 256, 2, 5), (8, (8, 4), 256, 3, 5)),
+                  (4, (4, 4, 2), 256, 2, 5), (8, (8, 4), 256, 3, 5),
+                  # thread per signal: one in-register radix-32 DFT, no exchange / no shuffle sums
+                  (32, (32,), 128, 1, 3), (32, (32,), 256, 1, 3), (32, (32,), 128, 2, 3),
+                  (8, (8, 4), 256, 2, 13), (8, (8, 4), 256, 4, 5), (8, (8, 4), 256, 4, 13),
+                  (32, (32,), 128, 2, 11)),
         6: _cands((8, (8, 8), 256, 1, 1), (8, (8, 8), 256, 1, 0), (16, (16, 4), 256, 1, 1),
                   (16, (16, 4), 256, 1, 0), (8, (8, 8), 256, 1, 3), (8, (8, 8), 256, 1, 2),
-                  (8, (8, 8), 256, 1, 5), (8, (8, 8), 256, 2, 5), (8, (8, 8), 256, 3, 5)),
+                  (8, (8, 8), 256, 1, 5), (8, (8, 8), 256, 2, 5), (8, (8, 8), 256, 3, 5),
+                  (32, (32, 2), 128, 1, 3), (32, (32, 2), 256, 1, 3), (16, (16, 4), 256, 1, 3),
+                  (16, (16, 4), 256, 2, 2)),
         7: _cands((16, (16, 8), 256, 1, 0), (16, (16, 8), 256, 1, 1), (8, (8, 8, 2), 256, 1, 0),
                   (16, (16, 8), 256, 3, 0), (16, (16, 8), 256, 1, 2), (16, (16, 8), 128, 4, 0)),
         8: _cands((16, (16, 16), 256, 1, 0), (16, (16, 16), 256, 3, 0), (8, (8, 8, 4), 256, 1, 0),
@@ -116,9 +122,12 @@ SINGLE_CANDIDATES = {
 # clean-data false alarms): fp32 N = 32 -> 2 CTAs/SM, N = 1024 -> 3 CTAs/SM,
 # N = 8192 -> E = 32 in 256-thread CTAs (in-place TMA prefetch), fp64 N = 2048
 # -> ping-pong exchange regions (STAGE 6); after the exchange-addressing
-# rewrite (profiles/tune_r02c_fp32.json) N = 64 -> TMA bulk prefetch (STAGE 2).
+# rewrite (profiles/tune_r02c_fp32.json) N = 64 -> TMA bulk prefetch (STAGE 2);
+# N = 32 -> e^T W row read from smem each tile (stage code 13: 0.420 -> 0.407
+# ms, profiles/tune_r02e_fp32.json; the thread-per-signal radix-32 variants
+# measured 0.436).
 SINGLE_CHOICE = {
-    "fp32": {1: 1, 2: 1, 3: 4, 4: 5, 5: 7, 6: 5, 7: 0, 8: 4, 9: 7, 10: 9, 11: 8, 12: 6, 13: 11},
+    "fp32": {1: 1, 2: 1, 3: 4, 4: 5, 5: 14, 6: 5, 7: 0, 8: 4, 9: 7, 10: 9, 11: 8, 12: 6, 13: 11},
     "fp64": {1: 1, 2: 2, 3: 3, 4: 7, 5: 5, 6: 4, 7: 0, 8: 4, 9: 6, 10: 4, 11: 8, 12: 4, 13: 2},
 }
 ELEM_BYTES = {"fp32": 8, "fp64": 16}
@@ -219,14 +228,15 @@ def single_configs(all_candidates=True):
                 ps, _ = choose_padding(n, e, radices, prec)
                 s = threads // tps
                 ex = (n + (n >> ps) + 1 if ps else n) if len(radices) > 1 else 0
-                st = n + 1 if c["stage"] in (1, 3) else (n if c["stage"] == 4 else 0)
-                ib = s * n if c["stage"] in (2, 3, 6) else 0  # TMA prefetch buffer
-                if c["stage"] == 5:  # per-signal rows into padded slots
+                ld = c["stage"] & 7  # load strategy (| 8: e^T W row from smem for short signals too)
+                st = n + 1 if ld in (1, 3) else (n if ld == 4 else 0)
+                ib = s * n if ld in (2, 3, 6) else 0  # TMA prefetch buffer
+                if ld == 5:  # per-signal rows into padded slots
                     ib = s * (n + 32 // ELEM_BYTES[prec])
                 # ABFT scratch: per-warp sums (TPS <= 32) or the deferred
                 # two-tile reduction pipeline (TPS >= 128: 2 x S x 5 x TPS partials + totals)
                 red = 10 * (threads // 32 + 1) + (10 * threads + 10 * s if tps >= 128 else 0)
-                regions = 2 if c["stage"] == 6 else 1  # ping-pong exchange regions
+                regions = 2 if ld == 6 else 1  # ping-pong exchange regions
                 smem = (ib + regions * s * max(ex, st)) * ELEM_BYTES[prec] + red * (ELEM_BYTES[prec] // 2)
                 out.append(dict(prec=prec, logn=logn, n=n, e=e, radices=radices, threads=threads,
                                 ps=ps, smem=smem, tps=tps, minb=c["minb"], stage=c["stage"],

@@ -291,9 +291,14 @@ __device__ __forceinline__ void stage_out(C<T>* __restrict__ dst, long long vali
     }
 }
 
-template <class T, int N, int E, int PS, int ABFT, int THREADS, int MINB, int STAGE, class Radices>
+template <class T, int N, int E, int PS, int ABFT, int THREADS, int MINB, int STAGE_CODE, class Radices>
 __global__ void __launch_bounds__(THREADS, MINB)
 fft_single_kernel(const __grid_constant__ SingleArgs<T> a) {
+    // STAGE_CODE = load strategy (below) | 8: the e^T W row read from shared
+    // memory every tile even for short signals (frees the registers the
+    // compiler would otherwise pin it in across tiles: occupancy)
+    constexpr int STAGE = STAGE_CODE & 7;
+    constexpr bool EW_SM_ALL = (STAGE_CODE & 8) != 0;
     using Eng = Engine<T, N, E, Radices>;
     constexpr int TPS = N / E;
     constexpr int S = THREADS / TPS;  // signals per CTA
@@ -478,7 +483,7 @@ fft_single_kernel(const __grid_constant__ SingleArgs<T> a) {
     // per-tile reads are then LDS instead of L1-hit LDGs (fp32 N = 2048:
     // 0.512 -> 0.491 ms; at 32 KB the lost occupancy costs more than it saves)
     // (not with the ping-pong regions, whose dynamic smem already sets the occupancy)
-    constexpr bool EWS = TFFT_EW_SMEM && TB && TPS >= 64 && N * (int)sizeof(C<T>) <= 16384 && !PP;
+    constexpr bool EWS = TFFT_EW_SMEM && TB && (TPS >= 64 || EW_SM_ALL) && N * (int)sizeof(C<T>) <= 16384 && !PP;
     __shared__ C<T> etw_sm[EWS ? N : 1];
     if constexpr (EWS) {
         for (int i = threadIdx.x; i < N; i += THREADS) etw_sm[i] = a.etw[i];

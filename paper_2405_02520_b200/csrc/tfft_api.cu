@@ -370,7 +370,7 @@ int launch_single_t(tfft_plan* p, const Launch& L, cudaStream_t st) {
     a.f_bit = L.f_bit;
     const int S = e->threads / e->tps;
     const long long tiles = (L.batch + S - 1) / S;
-    if (e->stage == 5) {  // rows as a 2-D tensor, box padded past the signal end
+    if ((e->stage & 7) == 5) {  // rows as a 2-D tensor, box padded past the signal end
         int rc2 = encode_single_tmap(&a.tmap, L.in, p->n, L.batch, (int)p->esize, S);
         if (rc2) return rc2;
     }
