@@ -162,7 +162,7 @@ def _cpu_jobs(sample_elems, shards_per_size):
     return jobs, total
 
 
-def cpu_reference(cores=None, single_elems=1 << 21, multi_elems=1 << 23):
+def cpu_reference(cores=None, single_elems=1 << 24, multi_elems=1 << 25):
     """The reference's CPU path (oracle port; butterflies by the reference's
     own compiled `_stockham` when oracle/_ref is built) over bounded samples
     of the C2 sweep, measured two ways:

@@ -234,8 +234,9 @@ def single_configs(all_candidates=True):
                 if ld == 5:  # per-signal rows into padded slots
                     ib = s * (n + 32 // ELEM_BYTES[prec])
                 # ABFT scratch: per-warp sums (TPS <= 32) or the deferred
-                # two-tile reduction pipeline (TPS >= 128: 2 x S x 5 x TPS partials + totals)
-                red = 10 * (threads // 32 + 1) + (10 * threads + 10 * s if tps >= 128 else 0)
+                # two-tile reduction pipeline (2 x S x 5 x TPS partials + totals)
+                # (sized for >= 64-thread signals: TFFT_DEFER_MIN may select the pipeline there)
+                red = 10 * (threads // 32 + 1) + (10 * threads + 10 * s if tps >= 64 else 0)
                 regions = 2 if ld == 6 else 1  # ping-pong exchange regions
                 smem = (ib + regions * s * max(ex, st)) * ELEM_BYTES[prec] + red * (ELEM_BYTES[prec] // 2)
                 out.append(dict(prec=prec, logn=logn, n=n, e=e, radices=radices, threads=threads,

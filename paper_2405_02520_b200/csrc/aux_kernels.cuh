@@ -97,6 +97,7 @@ __global__ void group_sums_kernel(const C<T>* __restrict__ xg, long long bs, lon
          k += (long long)gridDim.x * blockDim.x) {
         C<T> a = xg[k];
         double2 w = make_double2((double)a.x, (double)a.y);
+#pragma unroll 8
         for (long long b = 1; b < bs; ++b) {
             const C<T> v = xg[b * n + k];
             a = cadd<T>(a, v);
@@ -153,7 +154,8 @@ __global__ void group_sums_jobs_kernel(const C<T>* __restrict__ in, long long bs
     for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n;
          k += (long long)gridDim.x * blockDim.x) {
         C<T> a = xg[k];
-        for (long long b = 1; b < bs; ++b) a = cadd<T>(a, xg[b * n + k]);
+#pragma unroll 8
+        for (long long b = 1; b < bs; ++b) a = cadd<T>(a, xg[b * n + k]);  // 8 loads in flight, sum in order
         dst[k] = a;
     }
 }
@@ -163,7 +165,7 @@ __global__ void group_sums_jobs_kernel(const C<T>* __restrict__ in, long long bs
 // `scratch` and writes the chunk's (c_in, c_out, l1) partials; phase 2 (one
 // CTA per group) sums them in chunk order and decides; phase 3 commits the
 // verified groups chunk by chunk.
-constexpr int FIX_CHUNK = 2048;  // points per CTA in phase 1 / 3
+constexpr int FIX_CHUNK = 512;  // points per CTA in phase 1 / 3 (2 per thread: latency, not bandwidth)
 template <class T>
 __global__ void __launch_bounds__(256)
 fix_rebuild_kernel(const C<T>* __restrict__ in, const C<T>* __restrict__ out, long long n, long long bs,
@@ -182,12 +184,14 @@ fix_rebuild_kernel(const C<T>* __restrict__ in, const C<T>* __restrict__ out, lo
     for (long long k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
         C<T> others = mk<T>(T(0), T(0));
         bool first = true;
-        for (long long b = 0; b < bs; ++b) {
+#pragma unroll 8
+        for (long long b = 0; b < bs; ++b) {  // unconditional loads (8 in flight), sum in order
             const long long sg = job.first + b;
-            if (sg == job.flagged) continue;
             const C<T> v = out[sg * n + k];
-            others = first ? v : cadd<T>(others, v);
-            first = false;
+            if (sg != job.flagged) {
+                others = first ? v : cadd<T>(others, v);
+                first = false;
+            }
         }
         const C<T> f = csub<T>(w[k], others);
         fx[k] = f;
@@ -220,13 +224,28 @@ fix_rebuild_kernel(const C<T>* __restrict__ in, const C<T>* __restrict__ out, lo
 }
 
 template <class T>
-__global__ void fix_decide_kernel(long long chunks, const T* __restrict__ part, T delta, T abs_floor,
-                                  T floor_coef, FixJob* jobs) {
-    if (threadIdx.x != 0) return;
+__global__ void __launch_bounds__(256) fix_decide_kernel(long long chunks, const T* __restrict__ part, T delta,
+                                                         T abs_floor, T floor_coef, FixJob* jobs) {
+    // fixed-order parallel sum of the chunk partials: thread t takes chunks
+    // t, t + 256, ... in order, then a fixed tree (deterministic)
+    __shared__ T sh[256][5];
     T a[5] = {T(0), T(0), T(0), T(0), T(0)};
-    for (long long c = 0; c < chunks; ++c)
+    for (long long c = threadIdx.x; c < chunks; c += blockDim.x)
 #pragma unroll
         for (int i = 0; i < 5; ++i) a[i] = fadd(a[i], part[((long long)blockIdx.x * chunks + c) * 5 + i]);
+#pragma unroll
+    for (int i = 0; i < 5; ++i) sh[threadIdx.x][i] = a[i];
+    __syncthreads();
+    for (int w = blockDim.x / 2; w >= 1; w /= 2) {
+        if ((int)threadIdx.x < w) {
+#pragma unroll
+            for (int i = 0; i < 5; ++i) sh[threadIdx.x][i] = fadd(sh[threadIdx.x][i], sh[threadIdx.x + w][i]);
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x != 0) return;
+#pragma unroll
+    for (int i = 0; i < 5; ++i) a[i] = sh[0][i];
     const C<T> raw = mk<T>(fsub(a[0], a[2]), fsub(a[1], a[3]));
     const T fl = nanmax<T>(abs_floor, fmul(floor_coef, a[4]));
     const T den = nanmax<T>(cabs<T>(mk<T>(a[0], a[1])), fl);

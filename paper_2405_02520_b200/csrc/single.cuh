@@ -30,6 +30,9 @@ enum { AT_NONE = 0, AT_INPUT = 1, AT_PRESCALE = 2, AT_OUTPUT = 3 };
 #ifndef TFFT_EW_HOIST
 #define TFFT_EW_HOIST 1
 #endif
+#ifndef TFFT_DEFER_MIN
+#define TFFT_DEFER_MIN 128  // signals of >= this many threads use the smem partial pipeline
+#endif
 #ifndef TFFT_EW_SMEM
 #define TFFT_EW_SMEM 1
 #endif
@@ -414,8 +417,8 @@ fft_single_kernel(const __grid_constant__ SingleArgs<T> a) {
     // warps shuffle their sums fully, lanes 0 store them (parity-buffered), and
     // thread t == 0 adds the few warp totals after the next tile's barrier.
     constexpr bool TB = ABFT == ABFT_WANG || ABFT == ABFT_TABLE;  // threadblock-level checksums
-    constexpr bool DEFER1 = TB && TPS > 32 && TPS < 128;
-    constexpr bool DEFER = TB && TPS >= 128;
+    constexpr bool DEFER1 = TB && TPS > 32 && TPS < TFFT_DEFER_MIN;
+    constexpr bool DEFER = TB && TPS >= TFFT_DEFER_MIN && TPS > 32;
     bool pend = false, pend_live = false;
     long long pend_b = 0;
     unsigned pend_par = 0;

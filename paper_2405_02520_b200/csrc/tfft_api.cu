@@ -1165,8 +1165,9 @@ int correct_groups(tfft_plan* p, const void* in, void* out, int scheme, const vo
         }
         CU(cudaMemcpyAsync(p->d_jobs, jobs.data(), K * sizeof(FixJob), cudaMemcpyHostToDevice, st));
         // all K group sums in one launch, then one batched FFT of them
+        // one point per thread (the group loop is latency-bound: spread it wide)
         const unsigned gx = (unsigned)std::max<long long>(1, std::min<long long>((n + 255) / 256,
-                                                                               (4LL * p->num_sms + K - 1) / K));
+                                                                               (64LL * p->num_sms + K - 1) / K));
         if (p->prec == TFFT_FP32)
             tfft::note_launch(), group_sums_jobs_kernel<float><<<dim3(gx, (unsigned)K), 256, 0, st>>>((const float2*)in, p->bs, n,
                                                                                 p->d_jobs, (float2*)s0);
@@ -1183,14 +1184,14 @@ int correct_groups(tfft_plan* p, const void* in, void* out, int scheme, const vo
             tfft::note_launch(), fix_rebuild_kernel<float><<<g, 256, 0, st>>>((const float2*)in, (const float2*)out, n, p->bs,
                                                         (const float2*)ws0, (float2*)fx2, (const float2*)etw,
                                                         (const float2*)values, p->d_jobs, (float*)part);
-            tfft::note_launch(), fix_decide_kernel<float><<<(unsigned)K, 32, 0, st>>>(chunks, (const float*)part, (float)delta,
+            tfft::note_launch(), fix_decide_kernel<float><<<(unsigned)K, 256, 0, st>>>(chunks, (const float*)part, (float)delta,
                                                                 (float)abs_floor, 1e-6f, p->d_jobs);
             tfft::note_launch(), fix_commit_kernel<float><<<g, 256, 0, st>>>((float2*)out, n, (const float2*)fx2, p->d_jobs);
         } else {
             tfft::note_launch(), fix_rebuild_kernel<double><<<g, 256, 0, st>>>((const double2*)in, (const double2*)out, n, p->bs,
                                                          (const double2*)ws0, (double2*)fx2, (const double2*)etw,
                                                          (const double2*)values, p->d_jobs, (double*)part);
-            tfft::note_launch(), fix_decide_kernel<double><<<(unsigned)K, 32, 0, st>>>(chunks, (const double*)part, delta, abs_floor,
+            tfft::note_launch(), fix_decide_kernel<double><<<(unsigned)K, 256, 0, st>>>(chunks, (const double*)part, delta, abs_floor,
                                                                  1e-12, p->d_jobs);
             tfft::note_launch(), fix_commit_kernel<double><<<g, 256, 0, st>>>((double2*)out, n, (const double2*)fx2, p->d_jobs);
         }
