@@ -68,18 +68,22 @@ SINGLE_CANDIDATES = {
                    (8, (8, 8, 8, 4), 256, 3, 0), (16, (16, 16, 8), 512, 1, 0),
                    (16, (16, 16, 8), 256, 3, 2), (16, (16, 16, 8), 256, 2, 2),
                    (16, (16, 16, 8), 256, 2, 4), (32, (32, 32, 2), 128, 3, 0), (32, (32, 16, 4), 128, 3, 0),
-                   (32, (32, 16, 4), 128, 2, 6), (32, (32, 32, 2), 128, 2, 6), (16, (16, 16, 8), 256, 2, 6)),
+                   (32, (32, 16, 4), 128, 2, 6), (32, (32, 32, 2), 128, 2, 6), (16, (16, 16, 8), 256, 2, 6),
+                   (32, (32, 16, 4), 128, 3, 2), (32, (32, 16, 4), 128, 3, 4), (32, (32, 16, 4), 128, 2, 2),
+                   (32, (32, 16, 4), 128, 2, 4)),
         12: _cands((16, (16, 16, 16), 256, 2, 0), (16, (16, 16, 16), 256, 3, 0),
                    (8, (8, 8, 8, 8), 512, 2, 0), (16, (16, 16, 16), 512, 1, 0),
                    (16, (16, 16, 16), 256, 3, 2), (16, (16, 16, 16), 256, 2, 2),
                    (16, (16, 16, 16), 256, 2, 4), (32, (32, 32, 4), 128, 3, 0), (32, (32, 16, 8), 128, 3, 0),
-                   (16, (16, 16, 16), 256, 2, 6), (32, (32, 16, 8), 128, 2, 6)),
+                   (16, (16, 16, 16), 256, 2, 6), (32, (32, 16, 8), 128, 2, 6),
+                   (32, (32, 16, 8), 128, 3, 4), (32, (32, 16, 8), 128, 2, 4), (32, (32, 16, 8), 128, 3, 2)),
         13: _cands((16, (16, 16, 16, 2), 512, 2, 0), (32, (32, 16, 16), 256, 1, 0),
                    (16, (16, 16, 16, 2), 512, 1, 0), (8, (8, 8, 8, 8, 2), 1024, 1, 0),
                    (16, (16, 16, 16, 2), 512, 2, 2), (16, (16, 16, 16, 2), 512, 1, 2),
                    (16, (16, 16, 16, 2), 512, 2, 1), (16, (16, 16, 16, 2), 512, 2, 4),
                    (16, (16, 16, 16, 2), 512, 1, 4), (16, (16, 16, 16, 2), 512, 1, 6),
-                   (32, (32, 16, 16), 256, 1, 6), (32, (32, 16, 16), 256, 1, 4)),
+                   (32, (32, 16, 16), 256, 1, 6), (32, (32, 16, 16), 256, 1, 4),
+                   (32, (32, 16, 16), 256, 1, 2)),
     },
     "fp64": {
         1: _cands((2, (2,), 256, 1, 1), (2, (2,), 256, 1, 0), (2, (2,), 256, 1, 3)),
@@ -442,7 +446,7 @@ def _emit_pass(prec, cfgs):
             return (f"(const void*)&fft_pass_kernel<{t}, {c['l']}, {c['e']}, {c['u']}, {c['p']}, "
                     f"{kind}, {abft}, {c['minb']}, {c['pf']}, RList<{rl}>>")
         rows = [
-            f"{{{fn(0, 0)}, {fn(0, 1)}, {fn(0, 1)}}}",
+            f"{{{fn(0, 0)}, {fn(0, 1)}, {fn(0, 2)}}}",  # Wang: closed-form row; table encodings read it
             f"{{{fn(1, 0)}, nullptr, nullptr}}",
             f"{{{fn(2, 0)}, {fn(2, 1)}, {fn(2, 2)}}}",
         ]
@@ -500,6 +504,22 @@ def wang_etw_header():
             lines.append(f"    constexpr double t{R}[{R}] = {{{', '.join(repr(v) for v in vals)}}};")
         lines.append("    return R == 2 ? t2[r] : R == 4 ? t4[r] : R == 8 ? t8[r] : R == 16 ? t16[r] : t32[r];")
         lines.append("}")
+    # cot(m pi / E) for the closed-form e^T W of the multi-pass first pass
+    # (consecutive elements of a thread are pi/E apart in angle, multi.cuh)
+    try:
+        import mpmath as mp
+        mp.mp.dps = 50
+        cot = lambda m, e: float(mp.cot(mp.pi * m / e))  # noqa: E731
+    except ImportError:  # pragma: no cover
+        import numpy as np
+        cot = lambda m, e: float(1 / np.tan(np.longdouble(np.pi) * m / e))  # noqa: E731
+    lines.append("// cot(m pi / E), m = 1..E-1 (index 0 unused), rounded once from 50 digits.")
+    lines.append("__host__ __device__ constexpr double cot_pi_frac(int E, int m) {")
+    for e in (2, 4, 8, 16, 32):
+        vals = [0.0] + [cot(m, e) for m in range(1, e)]
+        lines.append(f"    constexpr double c{e}[{e}] = {{{', '.join(repr(v) for v in vals)}}};")
+    lines.append("    return E == 2 ? c2[m] : E == 4 ? c4[m] : E == 8 ? c8[m] : E == 16 ? c16[m] : c32[m];")
+    lines.append("}")
     lines.append("}  // namespace tfft")
     return "\n".join(lines) + "\n"
 

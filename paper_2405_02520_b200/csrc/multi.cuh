@@ -82,6 +82,56 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
         : "memory");
 }
 
+#ifndef TFFT_ETW_CF
+#define TFFT_ETW_CF 1  // Wang first pass: closed-form e^T W in registers (0: the n-element table)
+#endif
+
+// Closed form of the Wang input-side row (checked against the
+// table path in tests/test_gpu_etw.py):
+//   etw[n]     = (A / 2) (1 - i cot(pi k_n / (3N))),  k_n = (N + 3n) mod 3N,
+//   etw_inv[n] = (A / 2N)(1 - i cot(pi k_n / (3N))),  k_n = (N - 3n) mod 3N,
+// A = 1 - w3^N, k reduced to (-1.5N, 1.5N] (cot has period pi). In the first
+// pass element (column lo, row j) has n = lo + j N/L, i.e. angle
+// alpha_lo +- j pi / L: one exactly reduced cot per column and tile
+// (sincospi in double, by U threads, shared through smem), a per-launch smem
+// table of cot(j pi / L), and the addition formula
+// cot(a + b) = (cot a cot b - 1) / (cot a + cot b) per element. The formula
+// loses accuracy only near the pole of the sum; elements within 1/256 rad of
+// it (|k| < 3N / (256 pi), integer test) use the Laurent series of cot at 0
+// on the exactly reduced angle. Nothing is read from HBM.
+template <class T>
+__device__ __forceinline__ T fast_rcp(T d);
+template <>
+__device__ __forceinline__ float fast_rcp<float>(float d) { return __fdividef(1.0f, d); }
+template <>
+__device__ __forceinline__ double fast_rcp<double>(double d) {
+    double r = (double)__fdividef(1.0f, (float)d);  // |d| in [4e-3, 1e8]: a normal float
+    double e = __fma_rn(-d, r, 1.0);
+    r = __fma_rn(r, e, r);
+    e = __fma_rn(-d, r, 1.0);
+    return __fma_rn(r, e, r);  // two Newton steps: ~1e-16 relative
+}
+// k of column lo (exact, in (-1.5N, 1.5N]) and cot(pi k / 3N)
+template <class T>
+__device__ __forceinline__ void wang_col_base(long long lo, int N, bool inv, int& k, T& c) {
+    const int N3 = 3 * N, H = N3 / 2;
+    int kk = inv ? N - 3 * (int)lo : N + 3 * (int)lo;  // lo < N: one wrap at most
+    if (kk > H) kk -= N3;
+    else if (kk <= -H) kk += N3;
+    double sb, cb;
+    sincospi((double)kk / (double)N3, &sb, &cb);
+    k = kk;
+    c = (T)(cb / sb);  // k != 0: N is not a multiple of 3
+}
+// Laurent series of cot at 0: for the one element per thread that lies within
+// 1/256 rad of the pole (|k| < 3N / (256 pi))
+template <class T>
+__device__ __forceinline__ T cot_near_pole(int k, int N3) {
+    const T d = (T)k * (T)(3.14159265358979323846 / (double)N3);
+    const T d2 = d * d;
+    return fast_rcp<T>(d) - d * (T(1) / T(3) + d2 * (T(1) / T(45) + d2 * (T(2) / T(945))));
+}
+
 // Engine memory policy of a pass tile: [L][U] rows of stride RS, lane u.
 template <class T, int RS>
 struct RowMem {
@@ -111,7 +161,8 @@ fft_pass_kernel(const __grid_constant__ PassArgs<T> a) {
     // instead of one L2 round trip of per-element loads.
     constexpr bool BULK = PF == 2 || PF == 3 || PF == 4;
     constexpr bool TENSOR = (PF == 3 || PF == 4) && KIND != KIND_LAST;
-    constexpr bool ETW_TMA = PF == 4 && KIND == KIND_FIRST && ABFT != ABFT_OFF;
+    constexpr bool CF = KIND == KIND_FIRST && ABFT == ABFT_WANG && TFFT_ETW_CF;  // closed-form row
+    constexpr bool ETW_TMA = PF == 4 && KIND == KIND_FIRST && ABFT != ABFT_OFF && !CF;
     constexpr int BOXR = L < 256 ? L : 256;
     constexpr int SU = sizeof(T) == 4 ? L + 2 : L + 1;  // 16-byte aligned padded row
     // buffer size rounded to 16 elements so the second buffer stays 128-byte
@@ -125,6 +176,10 @@ fft_pass_kernel(const __grid_constant__ PassArgs<T> a) {
     C<T>* etile = tile + (PF ? 2 : 1) * BUFE;                   // 2 x ETWE
     T* red = reinterpret_cast<T*>(etile + 2 * ETWE);
     __shared__ unsigned long long bbar[2];
+    // closed-form row: cot(+-j pi / L) per launch, column bases per tile (parity buffered)
+    __shared__ T cf_cj[CF ? L : 1];
+    __shared__ T cf_cc[CF ? 2 * U : 1];
+    __shared__ int cf_kc[CF ? 2 * U : 1];
 
     const int u = threadIdx.x % U;
     const int t = threadIdx.x / U;
@@ -213,6 +268,28 @@ fft_pass_kernel(const __grid_constant__ PassArgs<T> a) {
     }
 
     const unsigned bbar_s = smem_u32(&bbar[0]);  // shared-window address, converted once
+    // closed-form row: column bases of tile tx (threads u < U, i.e. t == 0)
+    const int cf_n = (int)a.n;
+    const int cf_kap = (int)((double)(3 * cf_n) * (1.0 / (256.0 * 3.14159265358979323846))) + 1;
+    auto cf_col_base = [&](long long tx, unsigned par) {
+        long long bb, ts;
+        tile_of(tx, bb, ts);
+        int k;
+        T c;
+        wang_col_base<T>(ts * U + threadIdx.x, cf_n, a.inverse != 0, k, c);
+        cf_kc[par * U + threadIdx.x] = k;
+        cf_cc[par * U + threadIdx.x] = c;
+    };
+    if constexpr (CF) {
+        const double sg = a.inverse ? -1.0 : 1.0;
+        for (int j = threadIdx.x; j < L; j += THREADS) {
+            double sj, cj;
+            sincospi((double)j / (double)L, &sj, &cj);
+            cf_cj[j] = j ? (T)(sg * cj / sj) : T(0);
+        }
+        if (threadIdx.x < U && blockIdx.x < total) cf_col_base(blockIdx.x, 0);
+        __syncthreads();
+    }
     unsigned it = 0;
     for (long long tix = blockIdx.x; tix < total; tix += gridDim.x, ++it) {
         C<T>* cur = (PF && (it & 1)) ? tile + BUFE : tile;
@@ -240,8 +317,38 @@ fft_pass_kernel(const __grid_constant__ PassArgs<T> a) {
         // input-side ABFT row e^T W for this tile, requested before the tile
         // data is waited for so its latency overlaps (one batch of
         // independent loads, not one round trip per element)
-        C<T> ew[(KIND == KIND_FIRST && ABFT != ABFT_OFF) ? E : 1];
-        if constexpr (KIND == KIND_FIRST && ABFT != ABFT_OFF && !ETW_TMA) {
+        C<T> ew[(KIND == KIND_FIRST && ABFT != ABFT_OFF && !CF) ? E : 1];
+        T ct[CF ? E : 1];
+        if constexpr (CF) {
+            const unsigned par = it & 1;
+            const T cc = cf_cc[par * U + u];
+            // this thread's rows j = t + m TPS are pi/E apart in angle: at most
+            // one of them (m*) can lie within 1/256 rad of the pole; find it with
+            // integer arithmetic and patch it after the addition formula
+            const int N3 = 3 * cf_n, H = N3 / 2;
+            const int dk = (a.inverse ? -3 : 3) * (int)a.in_j;  // +-3 N / L per row
+            int kt = cf_kc[par * U + u] + dk * t;
+            if (kt > H) kt -= N3;
+            else if (kt <= -H) kt += N3;
+            const int dm = dk * TPS;  // +-3N / E per element
+            int ms = (int)llrint(-(double)kt / (double)dm);
+            ms = ((ms % E) + E) % E;
+            int km = kt + dm * ms;
+            if (km > H) km -= N3;
+            else if (km <= -H) km += N3;
+            const bool pole = km < cf_kap && km > -cf_kap && (t + ms * TPS) != 0;
+            const T cp = pole ? cot_near_pole<T>(km, N3) : T(0);
+#pragma unroll
+            for (int m = 0; m < E; ++m) {
+                const int j = t + m * TPS;
+                const T cj = cf_cj[j];
+                T cm = (cc * cj - T(1)) * fast_rcp<T>(cc + cj);
+                if (m == 0) cm = t == 0 ? cc : cm;
+                ct[m] = (pole && m == ms) ? cp : cm;
+            }
+            // the next tile's column bases (its readers run after this tile's trailing barrier)
+            if (threadIdx.x < U && tix + gridDim.x < total) cf_col_base(tix + gridDim.x, par ^ 1u);
+        } else if constexpr (KIND == KIND_FIRST && ABFT != ABFT_OFF && !ETW_TMA) {
             const C<T>* ep = a.etw + ibase + (long long)t * a.in_j;
             const long long es = (long long)TPS * a.in_j;
 #pragma unroll
@@ -303,8 +410,19 @@ fft_pass_kernel(const __grid_constant__ PassArgs<T> a) {
 #pragma unroll
             for (int k = 0; k < KA; ++k) ca[k] = la[k] = mk<T>(T(0), T(0));
 #pragma unroll
+            C<T> sa[CF ? KA : 1];  // closed form: ca = sum x, sa = sum x cot
+            if constexpr (CF) {
+#pragma unroll
+                for (int k = 0; k < KA; ++k) sa[k] = mk<T>(T(0), T(0));
+            }
+#pragma unroll
             for (int m = 0; m < E; ++m) {
-                ca[m % KA] = cmac<T>(ca[m % KA], v[m], ew[m]);
+                if constexpr (CF) {
+                    ca[m % KA] = cadd<T>(ca[m % KA], v[m]);
+                    sa[m % KA] = mk<T>(ffma(v[m].x, ct[m], sa[m % KA].x), ffma(v[m].y, ct[m], sa[m % KA].y));
+                } else {
+                    ca[m % KA] = cmac<T>(ca[m % KA], v[m], ew[m]);
+                }
                 la[m % KA] = cadd<T>(la[m % KA], cabs2<T>(v[m]));
             }
 #pragma unroll
@@ -313,9 +431,19 @@ fft_pass_kernel(const __grid_constant__ PassArgs<T> a) {
                 for (int k = 0; k < w; ++k) {
                     ca[k] = cadd<T>(ca[k], ca[k + w]);
                     la[k] = cadd<T>(la[k], la[k + w]);
+                    if constexpr (CF) sa[k] = cadd<T>(sa[k], sa[k + w]);
                 }
             }
-            const C<T> cin = ca[0], l1p = la[0];
+            C<T> cin = ca[0];
+            if constexpr (CF) {
+                // x . etw = (A / 2)(S0 - i S1), S0 = sum x, S1 = sum x cot; A = 1 - w3^N
+                // = (1.5, +-sqrt(3)/2) for N = 1 / 2 (mod 3); inverse: also / N
+                const T hs = T(0.8660254037844386467637232) * ((a.n % 3 == 1) ? T(1) : T(-1));
+                const T g = a.inverse ? T(0.5) / T(a.n) : T(0.5);
+                const C<T> u = mk<T>(fadd(ca[0].x, sa[0].y), fsub(ca[0].y, sa[0].x));
+                cin = cmul<T>(u, mk<T>(T(1.5) * g, hs * g));
+            }
+            const C<T> l1p = la[0];
             T s[3] = {cin.x, cin.y, fadd(l1p.x, l1p.y)};
             warp_partials<3>(s, red);  // summed by thread 0 after the tile's trailing barrier
         }

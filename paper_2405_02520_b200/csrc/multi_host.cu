@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -355,7 +356,16 @@ int multi_launch_t(MultiPlan& mp, const MultiLaunch& m, cudaStream_t st) {
         }
         int abft_v = ABFT_OFF;
         if (abft && kind == KIND_FIRST) {
-            abft_v = ABFT_WANG;  // input side: table row, any encoding
+            // input side: the Wang row in closed form (no table traffic) where it
+            // measured faster — L >= 256 and a small batch, whose table reads are
+            // a large share of the pass (profiles/etw_cf_r02.txt); otherwise, and
+            // for every other encoding, the e^T W row read from the table
+            static const long long cf_maxb = [] {
+                const char* e = getenv("TFFT_ETW_CF_MAXB");  // A/B override
+                return e ? atoll(e) : 8LL;
+            }();
+            const bool cf = m.abft == ABFT_WANG && d0 >= 256 && m.batch <= cf_maxb;
+            abft_v = cf ? ABFT_WANG : ABFT_TABLE;
             a.etw = (const C<T>*)m.etw;
             a.part = part_in;
         } else if (abft && kind == KIND_LAST) {

@@ -188,6 +188,38 @@ def overhead(out, reps=20):
         res["shape"] = {"n": n, "bs": bs, "groups": runs, "bytes": b * n * esz,
                         "call": "tfft_run_campaign (fused launch + per-run max rel read-back + correction)",
                         "fault": f"output bit {bit}, random signal/element/component per group"}
+        # the product entry point (what run_protected calls): tfft_run_protected
+        # on the same 1 GiB batch, clean vs one output fault
+        planf = fit_group_size(make_plan(n, prec, batch=b), b)
+        hf = native_plan(planf, 0)
+        one_f = _lib.Fault()
+        one_f.signal, one_f.element, one_f.component, one_f.bit = b // 2 + 3, n // 3, 0, bit
+        one_f.where = _lib.AT_OUTPUT
+
+        def call_rp(fault):
+            _lib.check(lib.tfft_run_protected(hf.handle, x.data_ptr(), y.data_ptr(), b,
+                                              _lib.SCHEME_CODE["two_sided_group"], delta, 0.0, row.data_ptr(),
+                                              None, ctypes.byref(fault) if fault is not None else None, 0,
+                                              ctypes.byref(rep), stream.cuda_stream), "tfft_run_protected")
+
+        rp = {}
+        for label, fault in (("clean", None), ("one_fault", one_f)):
+            for _ in range(3):
+                call_rp(fault)
+            ts = []
+            for _ in range(reps):
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                call_rp(fault)
+                e1.record(stream)
+                torch.cuda.synchronize()
+                ts.append(e0.elapsed_time(e1))
+            rp[label] = {"ms": round(statistics.median(ts), 4), "corrected": int(rep.n_corrected),
+                         "flagged": int(rep.n_flagged)}
+        rp["one_fault"]["overhead_pct"] = round(100 * (rp["one_fault"]["ms"] / rp["clean"]["ms"] - 1), 2)
+        rp["call"] = "tfft_run_protected (the run_protected entry point), one output fault in the launch"
+        res["run_protected"] = rp
         out["correction_overhead"][prec] = res
         print(prec, json.dumps({k: v for k, v in res.items() if k != "clocks"}), flush=True)
         del x, y
