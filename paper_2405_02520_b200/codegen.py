@@ -49,12 +49,15 @@ SINGLE_CANDIDATES = {
                   (16, (16, 4), 256, 1, 0), (8, (8, 8), 256, 1, 3), (8, (8, 8), 256, 1, 2),
                   (8, (8, 8), 256, 1, 5), (8, (8, 8), 256, 2, 5), (8, (8, 8), 256, 3, 5),
                   (32, (32, 2), 128, 1, 3), (32, (32, 2), 256, 1, 3), (16, (16, 4), 256, 1, 3),
-                  (16, (16, 4), 256, 2, 2)),
+                  (16, (16, 4), 256, 2, 2),
+                  # warp-shuffle transpose exchange (stage code | 16)
+                  (8, (8, 8), 256, 1, 18), (8, (8, 8), 256, 3, 21)),
         7: _cands((16, (16, 8), 256, 1, 0), (16, (16, 8), 256, 1, 1), (8, (8, 8, 2), 256, 1, 0),
                   (16, (16, 8), 256, 3, 0), (16, (16, 8), 256, 1, 2), (16, (16, 8), 128, 4, 0)),
         8: _cands((16, (16, 16), 256, 1, 0), (16, (16, 16), 256, 3, 0), (8, (8, 8, 4), 256, 1, 0),
                   (16, (16, 16), 256, 1, 1), (16, (16, 16), 256, 1, 2), (16, (16, 16), 256, 3, 2),
-                  (16, (16, 16), 128, 4, 0), (16, (16, 16), 128, 4, 2)),
+                  (16, (16, 16), 128, 4, 0), (16, (16, 16), 128, 4, 2),
+                  (16, (16, 16), 256, 1, 18), (16, (16, 16), 256, 1, 16)),
         9: _cands((16, (16, 16, 2), 256, 2, 0), (32, (32, 16), 256, 1, 0),
                   (8, (8, 8, 8), 256, 3, 0), (16, (16, 16, 2), 256, 3, 0),
                   (16, (16, 16, 2), 256, 2, 2), (8, (8, 8, 8), 256, 3, 2), (32, (32, 16), 256, 2, 0),
@@ -63,7 +66,7 @@ SINGLE_CANDIDATES = {
                    (16, (16, 16, 4), 256, 3, 0), (8, (8, 8, 8, 2), 256, 2, 0),
                    (16, (16, 16, 4), 512, 1, 0), (16, (16, 16, 4), 256, 3, 2),
                    (16, (16, 16, 4), 256, 2, 2), (32, (32, 32), 256, 2, 0), (32, (32, 32), 128, 2, 0),
-                   (32, (32, 32), 128, 3, 0)),
+                   (32, (32, 32), 128, 3, 0), (32, (32, 32), 128, 3, 16)),
         11: _cands((16, (16, 16, 8), 256, 2, 0), (16, (16, 16, 8), 256, 3, 0),
                    (8, (8, 8, 8, 4), 256, 3, 0), (16, (16, 16, 8), 512, 1, 0),
                    (16, (16, 16, 8), 256, 3, 2), (16, (16, 16, 8), 256, 2, 2),
@@ -129,9 +132,11 @@ SINGLE_CANDIDATES = {
 # rewrite (profiles/tune_r02c_fp32.json) N = 64 -> TMA bulk prefetch (STAGE 2);
 # N = 32 -> e^T W row read from smem each tile (stage code 13: 0.420 -> 0.407
 # ms, profiles/tune_r02e_fp32.json; the thread-per-signal radix-32 variants
-# measured 0.436).
+# measured 0.436); N = 2048 / 4096 -> E = 32 in 128-thread CTAs, 3 per SM, with
+# the in-place TMA prefetch (0.473 -> 0.423 / 0.444 -> 0.424 ms,
+# profiles/tune_r02f_fp32.json).
 SINGLE_CHOICE = {
-    "fp32": {1: 1, 2: 1, 3: 4, 4: 5, 5: 14, 6: 5, 7: 0, 8: 4, 9: 7, 10: 9, 11: 8, 12: 6, 13: 11},
+    "fp32": {1: 1, 2: 1, 3: 4, 4: 5, 5: 14, 6: 5, 7: 0, 8: 4, 9: 7, 10: 9, 11: 13, 12: 11, 13: 11},
     "fp64": {1: 1, 2: 2, 3: 3, 4: 7, 5: 5, 6: 4, 7: 0, 8: 4, 9: 6, 10: 4, 11: 8, 12: 4, 13: 2},
 }
 ELEM_BYTES = {"fp32": 8, "fp64": 16}

@@ -44,6 +44,7 @@ struct SmemLen { static constexpr int v = (PS == 0) ? L : L + (L >> PS) + 1; };
 template <class T, int TPS, int PS>
 struct SliceMem {
     static constexpr int kPS = PS;
+    static constexpr bool kShuffle = false;
     C<T>* base;
     // p = padidx<PS>(i): the engine computes padded indices (mostly per-thread
     // base + compile-time offset), the policy maps them to an address
@@ -56,6 +57,37 @@ struct SliceMem {
     __device__ __forceinline__ void release() const { sync(); }
     __device__ __forceinline__ void after_last_exchange() const {}
 };
+// SliceMem whose radix-E -> radix-E exchange (the full transpose of a
+// two-pass signal with E = TPS = R) runs on warp shuffles instead (the
+// paper's warp-level stage); any other exchange still goes through smem.
+template <class T, int TPS, int PS>
+struct ShflSliceMem : SliceMem<T, TPS, PS> {
+    static constexpr bool kShuffle = true;
+};
+
+// In-warp transpose of an E x E block (lanes t of one signal x registers):
+// log2 E rounds, each swapping one lane-index bit with the same register-
+// index bit: per register pair one 64-bit xor shuffle and the selects around
+// it. Afterwards lane t holds what lane m held in register t, in register m.
+template <class T, int E>
+__device__ __forceinline__ void shfl_transpose(C<T> (&v)[E], int t) {
+#pragma unroll
+    for (int mask = 1; mask < E; mask <<= 1) {
+        const bool hi = (t & mask) != 0;
+#pragma unroll
+        for (int r0 = 0; r0 < E; ++r0) {
+            if (r0 & mask) continue;
+            const int r1 = r0 | mask;
+            const C<T> send = hi ? v[r0] : v[r1];
+            C<T> recv;
+            recv.x = __shfl_xor_sync(0xffffffffu, send.x, mask);
+            recv.y = __shfl_xor_sync(0xffffffffu, send.y, mask);
+            v[r0] = hi ? recv : v[r0];
+            v[r1] = hi ? v[r1] : recv;
+        }
+    }
+}
+
 // Two alternating exchange regions (ping-pong): exchange k puts into and gets
 // from region `cur`, then switches, so the next exchange never writes what a
 // slower thread may still be reading and the trailing barrier of every
@@ -72,6 +104,7 @@ struct PingPongMem {
     Hook hook;
     mutable bool first = true;
     static constexpr int kPS = PS;
+    static constexpr bool kShuffle = false;
     __device__ __forceinline__ void putp(int p, C<T> v) const { (*cur)[p] = v; }
     __device__ __forceinline__ C<T> getp(int p) const { return (*cur)[p]; }
     __device__ __forceinline__ void sync() const {
@@ -86,6 +119,7 @@ struct PingPongMem {
 template <class T, int U, int PS>
 struct TileMem {
     static constexpr int kPS = PS;
+    static constexpr bool kShuffle = false;
     C<T>* base;
     int u;
     __device__ __forceinline__ void putp(int p, C<T> v) const { base[p * U + u] = v; }
@@ -216,7 +250,10 @@ struct Engine {
 #pragma unroll
             for (int r = 0; r < R; ++r) v[q + r * SUB] = a[r];
         }
-        if constexpr (sizeof...(Rest) > 0) {
+        if constexpr (sizeof...(Rest) > 0 && Mem::kShuffle && Ns == 1 && R == E && TPS == E) {
+            shfl_transpose<T, E>(v, t);  // warp-level stage: no shared memory, no barrier
+            passes<Ns * R>(v, mem, t, tw, chk, RList<Rest...>{});
+        } else if constexpr (sizeof...(Rest) > 0) {
             // padded indices: one per-thread base and compile-time offsets
             // whenever the stride is a multiple of the padding period (then
             // pad(b + k) = pad(b) + pad(k) exactly), else per element

@@ -136,6 +136,7 @@ __device__ __forceinline__ T cot_near_pole(int k, int N3) {
 template <class T, int RS>
 struct RowMem {
     static constexpr int kPS = 0;
+    static constexpr bool kShuffle = false;
     C<T>* base;
     int u;
     __device__ __forceinline__ void putp(int i, C<T> v) const { base[i * RS + u] = v; }

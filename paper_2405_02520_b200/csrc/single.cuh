@@ -302,6 +302,7 @@ fft_single_kernel(const __grid_constant__ SingleArgs<T> a) {
     // compiler would otherwise pin it in across tiles: occupancy)
     constexpr int STAGE = STAGE_CODE & 7;
     constexpr bool EW_SM_ALL = (STAGE_CODE & 8) != 0;
+    constexpr bool SHFL = (STAGE_CODE & 16) != 0;  // warp-shuffle transpose stage (E = TPS = radix)
     using Eng = Engine<T, N, E, Radices>;
     constexpr int TPS = N / E;
     constexpr int S = THREADS / TPS;  // signals per CTA
@@ -640,6 +641,10 @@ fft_single_kernel(const __grid_constant__ SingleArgs<T> a) {
                 }
             };
             const SliceMemHook<T, TPS, PS, decltype(refill)> mem{{sm}, refill};
+            if constexpr (ABFT == ABFT_THREAD) Eng::run(v, mem, t, a.tw, tchk);
+            else Eng::run(v, mem, t, a.tw);
+        } else if constexpr (SHFL) {
+            const ShflSliceMem<T, TPS, PS> mem{{sm}};
             if constexpr (ABFT == ABFT_THREAD) Eng::run(v, mem, t, a.tw, tchk);
             else Eng::run(v, mem, t, a.tw);
         } else {
