@@ -72,9 +72,11 @@ def main():
             small = torch.randn(64, n, dtype=dt, device="cuda")
             ref = np.fft.fft(small.cpu().numpy().astype(np.complex128), axis=-1)
             delta = args.delta if args.delta is not None else (1e-2 if prec == "fp32" else 1e-9)
-            nv = lib.tfft_tune_variants(pc, logn)
-            for v in range(nv):
-                _lib.check(lib.tfft_tune_select(pc, logn, v))
+            from paper_2405_02520_b200 import codegen
+            ncand = len(codegen.SINGLE_CANDIDATES[prec][logn])
+            for v in range(ncand):
+                if lib.tfft_tune_select(pc, logn, v) != 0:
+                    continue  # not compiled in this (size-restricted) tuning build
                 out = torch.empty_like(small)
                 _lib.check(lib.tfft_execute(h.handle, small.data_ptr(), out.data_ptr(), 64, 0, sp))
                 got = out.cpu().numpy().astype(np.complex128)
