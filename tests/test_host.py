@@ -156,3 +156,60 @@ def test_codegen_configs_are_consistent():
             eb = codegen.ELEM_BYTES[c["prec"]]
             assert (codegen.smem_cost(c["n"], c["e"], c["radices"], c["ps"], eb)
                     <= codegen.smem_cost(c["n"], c["e"], c["radices"], 0, eb))
+
+
+def _cf_row(n, L, inverse):
+    """A float64 restatement of the device's closed-form Wang row (multi.cuh:
+    wang_col_base / the per-launch cot(j pi/L) table / the addition formula /
+    the one Laurent-patched pole element per thread), for the first pass of
+    an n-point transform with stage length L, one thread per (column, t) and
+    E = 16 rows per thread (TPS = L / 16)."""
+    n3, h = 3 * n, 3 * n // 2
+    r0 = n // L
+    E = min(16, L)
+    tps = L // E
+    kap = int(n3 * (1.0 / (256.0 * math.pi))) + 1
+    cot = np.zeros(n)
+    cj = np.array([0.0] + [(-1 if inverse else 1) * math.cos(math.pi * j / L) / math.sin(math.pi * j / L)
+                           for j in range(1, L)])
+    dk = (-3 if inverse else 3) * r0
+    for lo in range(r0):
+        kk = n - 3 * lo if inverse else n + 3 * lo
+        kk = kk - n3 if kk > h else (kk + n3 if kk <= -h else kk)
+        cc = math.cos(math.pi * kk / n3) / math.sin(math.pi * kk / n3)
+        for t in range(tps):
+            kt = kk + dk * t
+            kt = kt - n3 if kt > h else (kt + n3 if kt <= -h else kt)
+            dm = dk * tps
+            ms = int(round(-kt / dm)) % E
+            km = kt + dm * ms
+            km = km - n3 if km > h else (km + n3 if km <= -h else km)
+            pole = -kap < km < kap and (t + ms * tps) != 0
+            for m in range(E):
+                j = t + m * tps
+                c = cc if j == 0 else (cc * cj[j] - 1.0) / (cc + cj[j])
+                if pole and m == ms:
+                    d = km * math.pi / n3
+                    c = 1 / d - d * (1 / 3 + d * d * (1 / 45 + d * d * 2 / 945))
+                cot[lo + j * r0] = c
+    return cot
+
+
+@pytest.mark.parametrize("n,L", [(1 << 12, 64), (1 << 14, 128), (1 << 16, 256)])
+@pytest.mark.parametrize("inverse", [False, True])
+def test_closed_form_etw_matches_reference_row(n, L, inverse):
+    """The first pass's closed-form input-side checksum x . etw =
+    (A/2)(S0 - i S1), S1 = sum x cot (A = 1 - w3^n, inverse / n), against the
+    reference's FFT-computed row (abft/encoding.py:58-62 via the oracle)."""
+    enc = P.encoding_for("wang", n, "c")
+    row = enc.etw_inv if inverse else enc.etw
+    cot = _cf_row(n, L, inverse)
+    rng = np.random.default_rng([n, L])
+    x = rng.standard_normal((4, n)) + 1j * rng.standard_normal((4, n))
+    s0 = x.sum(axis=1)
+    s1 = (x * cot).sum(axis=1)
+    hs = 0.8660254037844386 * (1 if n % 3 == 1 else -1)
+    g = 0.5 / n if inverse else 0.5
+    cin = (s0.real + s1.imag + 1j * (s0.imag - s1.real)) * complex(1.5 * g, hs * g)
+    ref = x @ row
+    assert np.max(np.abs(cin - ref) / np.abs(ref)) < 1e-12
