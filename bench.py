@@ -1,11 +1,12 @@
 """Benchmark: BASELINE.json configs[1] (C2) — the FP32 single-kernel FFT sweep
 N = 2^3 .. 2^13, a 1 GiB batch per size per GPU, two-sided ABFT on
 (two_sided_group) — plus the FP64 multi-pass leg C3 (N = 2^20 .. 2^25, 2 GiB
-per GPU), ABFT-off and cuFFT (torch.fft) comparisons, and the reference's CPU
-path timed beside it.
+per GPU), the C5 sweep (FP32 and FP64, N = 2^10 .. 2^25, 1 GiB per size per
+GPU: the shape of the 1/2/4/8-GPU scaling runs), ABFT-off and cuFFT
+(torch.fft) comparisons, and the reference's CPU path timed beside it.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--strong] [--skip-cpu] [--skip-c3]
+                    [--strong] [--skip-cpu] [--skip-c3] [--skip-c5]
 
 One step = one protected pass of the hot path over every size of the C2
 sweep (11 fused launches, 11 GiB in + 11 GiB out per GPU; every size writes
@@ -42,6 +43,7 @@ sys.path.insert(0, ROOT)
 METRIC = "batched FFT GFLOP/s & HBM GB/s (FP32/FP64, ABFT on) vs roofline; ABFT overhead %"
 SIZES = list(range(3, 14))            # C2: log2 N
 C3_SIZES = list(range(20, 26))        # C3: log2 N (fp64, multi-pass)
+C5_SIZES = list(range(10, 26))        # C5: log2 N, both precisions (the 1/2/4/8-GPU sweep)
 BATCH_BYTES = 1 << 30                 # C2: per size per GPU (complex64 input)
 C3_BYTES = 2 << 30                    # C3: per size per GPU (complex128 input)
 WORKLOAD = ("C2: FP32 single-kernel FFT sweep N=2^3..2^13, 1 GiB complex64 batch per size "
@@ -427,6 +429,35 @@ def run_ours(args, rank, world, local_rank):
                   launches=launches3, steps=steps3)
         del x3
 
+    # ---------------------------------------------------------------- C5
+    # BASELINE configs[4]: the batch-sharded FP32 / FP64 sweep N = 2^10..2^25,
+    # 1 GiB per size per GPU (weak; --strong: 1 GiB per size in total),
+    # two-sided ABFT on; time = max over ranks
+    c5 = None
+    if not args.skip_c5:
+        if args.skip_c3:
+            for c in cases:
+                c.pop("y", None)
+            x = None
+        torch.cuda.empty_cache()
+        c5 = {}
+        for prec in ("fp32", "fp64"):
+            esz = 8 if prec == "fp32" else 16
+            td = torch.complex64 if prec == "fp32" else torch.complex128
+            c5_bytes = BATCH_BYTES // share
+            x5 = torch.randn(c5_bytes // esz, dtype=td, device=dev,
+                             generator=torch.Generator(device=dev).manual_seed(5555 + rank))
+            cases5 = _cases(prec, C5_SIZES, c5_bytes, dev, local_rank)
+            d5 = 1e-4 if prec == "fp32" else 1e-9
+            for _ in range(2):
+                step(cases5, x5, "two_sided_group", d5)
+            ms5, per5, cnt5, mx5, clk5, l5 = timed(cases5, x5, "two_sided_group", d5, 3)
+            c5[prec] = dict(cases=cases5, per=per5, ms=max_over_ranks(ms5), clk=clk5, cnt=cnt5, launches=l5)
+            for c in cases5:
+                c.pop("y", None)
+            del x5
+            torch.cuda.empty_cache()
+
     if rank != 0:
         return
     hbm, peak_kind = peaks()
@@ -511,6 +542,24 @@ def run_ours(args, rank, world, local_rank):
                                "unrecoverable": int(c3["cnt"][2]), "max_rel_discrepancy": c3["mx"]},
             "sweep": rows,
         }
+    c5_out = None
+    if c5 is not None:
+        c5_out = {"workload": ("C5: batch-sharded FP32/FP64 sweep N=2^10..2^25, "
+                               f"{'1 GiB in total' if args.strong else '1 GiB per GPU'} per size, "
+                               "two_sided_group ABFT on; time = max over ranks"), "unit": "GFLOP/s"}
+        for prec, r in c5.items():
+            esz = 8 if prec == "fp32" else 16
+            rows = []
+            for i, c in enumerate(r["cases"]):
+                on = statistics.median(r["per"][i])
+                per_pass = 2.0 * c["b"] * c["n"] * esz
+                rows.append({"n": c["n"], "batch": c["b"], "passes": c["passes"], "ms": round(on, 4),
+                             "gflops": round(flops(c["n"], c["b"]) / on / 1e6, 1),
+                             "frac_per_executed_pass": round(c["passes"] * per_pass / on / 1e6 / hbm, 4)})
+            c5_out[prec] = {
+                "value": round(world * sum(flops(c["n"], c["b"]) for c in r["cases"]) / (r["ms"] / 1000) / 1e9, 1),
+                "ms_per_step": round(r["ms"], 4), "steps": 3, "gpu_launches": int(r["launches"]),
+                "clocks": r["clk"], "flagged": int(r["cnt"][0]), "sizes": rows}
     line = {
         "metric": METRIC,
         "value": round(step_flops / (ms_step / 1000) / 1e9, 1),
@@ -548,6 +597,7 @@ def run_ours(args, rank, world, local_rank):
                            "reduced_with": "nccl all_reduce per step" if world > 1 else "local"},
         "sweep": sweep,
         "c3": c3_out,
+        "c5": c5_out,
     }
     print(json.dumps(line), flush=True)
 
@@ -627,6 +677,7 @@ def main():
     ap.add_argument("--strong", action="store_true", help="fixed global batch (1 GiB per size) split over the ranks")
     ap.add_argument("--skip-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--skip-c3", action="store_true", help="skip the FP64 C3 leg")
+    ap.add_argument("--skip-c5", action="store_true", help="skip the C5 FP32/FP64 2^10..2^25 sweep")
     args = ap.parse_args()
     if "WORLD_SIZE" in os.environ:  # torchrun
         _run(args, int(os.environ.get("RANK", "0")), int(os.environ["WORLD_SIZE"]),
