@@ -354,7 +354,9 @@ PASS_CANDIDATES = {
                (16, (16, 16), 8, 2, 3), (8, (8, 8, 4), 8, 2, 3), (16, (16, 16), 8, 2, 4)),
         9: _pc((8, (8, 8, 8), 8, 1, 0), (8, (8, 8, 8), 4, 2, 1), (16, (16, 16, 2), 4, 2, 1),
                (8, (8, 8, 8), 8, 1, 1), (8, (8, 8, 8), 8, 1, 2), (8, (8, 8, 8), 4, 2, 2),
-               (8, (8, 8, 8), 8, 1, 3), (8, (8, 8, 8), 4, 2, 3)),
+               (8, (8, 8, 8), 8, 1, 3), (8, (8, 8, 8), 4, 2, 3),
+               (16, (16, 16, 2), 4, 2, 2), (16, (16, 16, 2), 8, 1, 2), (32, (32, 16), 4, 2, 2),
+               (32, (32, 16), 8, 1, 2), (32, (32, 16), 4, 3, 2)),
         10: _pc((8, (8, 8, 8, 2), 8, 1, 0), (8, (8, 8, 8, 2), 4, 2, 1), (16, (16, 16, 4), 4, 1, 1),
                 (16, (16, 16, 4), 2, 2, 1), (8, (8, 8, 8, 2), 4, 1, 2), (8, (8, 8, 8, 2), 2, 2, 2),
                 (8, (8, 8, 8, 2), 4, 1, 3), (8, (8, 8, 8, 2), 2, 2, 3)),

@@ -73,10 +73,12 @@ def main():
                 kind = 0 if k == 0 else (2 if k == nst - 1 else 1)
                 if (logl, kind) in best:
                     continue
-                nv = lib.tfft_tune_pass_variants(pc, logl)
+                from paper_2405_02520_b200 import codegen
+                ncand = len(codegen.PASS_CANDIDATES[prec].get(logl, []))
                 timings = []
-                for v in range(nv):
-                    _lib.check(lib.tfft_tune_pass_select(pc, logl, kind, v))
+                for v in range(ncand):
+                    if lib.tfft_tune_pass_select(pc, logl, kind, v) != 0:
+                        continue  # not compiled in this build
                     out = torch.empty_like(small)
                     try:
                         _lib.check(lib.tfft_execute(h.handle, small.data_ptr(), out.data_ptr(), 2, 0, sp))
