@@ -6,7 +6,7 @@ GPU: the shape of the 1/2/4/8-GPU scaling runs), ABFT-off and cuFFT
 (torch.fft) comparisons, and the reference's CPU path timed beside it.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--strong] [--skip-cpu] [--skip-c3] [--skip-c5]
+                    [--strong] [--skip-cpu] [--skip-c1] [--skip-c3] [--skip-c5]
 
 One step = one protected pass of the hot path over every size of the C2
 sweep (11 fused launches, 11 GiB in + 11 GiB out per GPU; every size writes
@@ -408,6 +408,57 @@ def run_ours(args, rank, world, local_rank):
                    "fused transform / D2H streamed in 32 MiB group-aligned chunks on three streams")}
     del xh
 
+    # ---------------------------------------------------------------- C1
+    # BASELINE configs[0] (the reference's own CPU-runnable case): FP32
+    # N = 1024, batch 256, two-sided, no faults — a 4 MiB latency case: per
+    # call wall time of the public run_protected (device tensors; numpy in /
+    # out) and the fused launch alone (events), medians of 200 calls
+    c1 = None
+    if not args.skip_c1:
+        from paper_2405_02520_b200 import make_plan, run_protected
+        from paper_2405_02520_b200.abft import make_encoding
+        from paper_2405_02520_b200.fft_core import fit_group_size
+        from paper_2405_02520_b200.fft_core.plan import native_plan
+        n1, b1 = 1024, 256
+        x1 = np.random.default_rng(rank).standard_normal((b1, 2 * n1)).view(np.complex128).astype(np.complex64)
+        plan1 = fit_group_size(make_plan(n1, "fp32", batch=b1), b1)
+        tw1 = build_twiddles(plan1)
+        xd1 = torch.from_numpy(x1).to(dev)
+        clk1 = ClockSampler(local_rank)
+        c1 = {"workload": "C1: FP32 N=1024 batch=256 two_sided_group, no faults (4 MiB, fits L2: latency)"}
+        clk1.start()
+        for name, inp in (("device_api_us", xd1), ("numpy_api_us", x1)):
+            for _ in range(20):
+                run_protected(plan1, tw1, inp, Scheme.TWO_SIDED_GROUP, cfg)
+            ts = []
+            for _ in range(200):
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                run_protected(plan1, tw1, inp, Scheme.TWO_SIDED_GROUP, cfg)
+                torch.cuda.synchronize()
+                ts.append((time.perf_counter() - t0) * 1e6)
+            c1[name] = round(statistics.median(ts), 1)
+        h1 = native_plan(plan1, local_rank)
+        row1 = make_encoding("wang", n1).device_row(torch.complex64)
+        y1 = torch.empty_like(xd1)
+        rep1 = Report(_lib).rep
+        ts = []
+        for i in range(220):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            _lib.check(lib.tfft_protect_launch(h1.handle, xd1.data_ptr(), y1.data_ptr(), b1, 3, 1e-4, 0.0,
+                                               row1.data_ptr(), None, None, 0, ctypes.byref(rep1), sp), "c1")
+            e1.record(stream)
+            torch.cuda.synchronize()
+            _lib.check(lib.tfft_protect_finish(h1.handle, xd1.data_ptr(), y1.data_ptr(), b1, 3, 1e-4, 0.0,
+                                               row1.data_ptr(), None, 0, ctypes.byref(rep1), sp), "c1")
+            if i >= 20:
+                ts.append(e0.elapsed_time(e1) * 1e3)
+        c1["fused_launch_us"] = round(statistics.median(ts), 1)
+        c1["clocks"] = clk1.stop()
+        c1["gflops_device_api"] = round(flops(n1, b1) / (c1["device_api_us"] * 1e-6) / 1e9, 1)
+        del xd1, y1
+
     # ---------------------------------------------------------------- C3
     c3 = None
     if not args.skip_c3:
@@ -596,6 +647,7 @@ def run_ours(args, rank, world, local_rank):
                            "max_rel_discrepancy": max_rel,
                            "reduced_with": "nccl all_reduce per step" if world > 1 else "local"},
         "sweep": sweep,
+        "c1": c1,
         "c3": c3_out,
         "c5": c5_out,
     }
@@ -678,6 +730,7 @@ def main():
     ap.add_argument("--skip-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--skip-c3", action="store_true", help="skip the FP64 C3 leg")
     ap.add_argument("--skip-c5", action="store_true", help="skip the C5 FP32/FP64 2^10..2^25 sweep")
+    ap.add_argument("--skip-c1", action="store_true", help="skip the C1 latency leg")
     args = ap.parse_args()
     if "WORLD_SIZE" in os.environ:  # torchrun
         _run(args, int(os.environ.get("RANK", "0")), int(os.environ["WORLD_SIZE"]),

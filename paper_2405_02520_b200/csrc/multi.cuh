@@ -410,7 +410,6 @@ fft_pass_kernel(const __grid_constant__ PassArgs<T> a) {
             C<T> ca[KA], la[KA];  // la: l1 upper bound sum(|re| + |im|), see abft_decide
 #pragma unroll
             for (int k = 0; k < KA; ++k) ca[k] = la[k] = mk<T>(T(0), T(0));
-#pragma unroll
             C<T> sa[CF ? KA : 1];  // closed form: ca = sum x, sa = sum x cot
             if constexpr (CF) {
 #pragma unroll
