@@ -127,8 +127,9 @@ SINGLE_CANDIDATES = {
 # Source: tools/tune.py on a B200, ABFT on, 1 GiB batches (profiles/tune_r01.json).
 # Round 2 (profiles/tune_r02_fp32.json, tune_r02_fp64.json; timed at a delta with no
 # clean-data false alarms): fp32 N = 32 -> 2 CTAs/SM, N = 1024 -> 3 CTAs/SM,
-# N = 8192 -> E = 32 in 256-thread CTAs (in-place TMA prefetch), fp64 N = 2048
-# -> ping-pong exchange regions (STAGE 6); after the exchange-addressing
+# N = 8192 -> E = 32 in 256-thread CTAs (in-place TMA prefetch); fp64: the
+# full retune after the addressing rewrite left every choice within 1-2 %
+# (profiles/tune_r02h_fp64.json; N = 2048 back to 3 CTAs/SM, direct loads); after the exchange-addressing
 # rewrite (profiles/tune_r02c_fp32.json) N = 64 -> TMA bulk prefetch (STAGE 2);
 # N = 32 -> e^T W row read from smem each tile (stage code 13: 0.420 -> 0.407
 # ms, profiles/tune_r02e_fp32.json; the thread-per-signal radix-32 variants
@@ -137,7 +138,7 @@ SINGLE_CANDIDATES = {
 # profiles/tune_r02f_fp32.json).
 SINGLE_CHOICE = {
     "fp32": {1: 1, 2: 1, 3: 4, 4: 5, 5: 14, 6: 5, 7: 0, 8: 4, 9: 7, 10: 9, 11: 13, 12: 11, 13: 11},
-    "fp64": {1: 1, 2: 2, 3: 3, 4: 7, 5: 5, 6: 4, 7: 0, 8: 4, 9: 6, 10: 4, 11: 8, 12: 4, 13: 2},
+    "fp64": {1: 1, 2: 2, 3: 3, 4: 7, 5: 5, 6: 4, 7: 0, 8: 4, 9: 6, 10: 4, 11: 5, 12: 4, 13: 2},
 }
 ELEM_BYTES = {"fp32": 8, "fp64": 16}
 CTYPE = {"fp32": "float", "fp64": "double"}
