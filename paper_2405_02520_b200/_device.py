@@ -16,9 +16,19 @@ _TORCH = {np.dtype(np.complex64): torch.complex64, np.dtype(np.complex128): torc
 _NUMPY = {torch.complex64: np.complex64, torch.complex128: np.complex128}
 
 
+_CUDA_OK = False
+_INIT = False
+
+
 def require_cuda():
+    # torch.cuda.is_available() re-reads the environment and NVML state on every
+    # call (~10 us on the C1 latency path); once a device was seen, stay true
+    global _CUDA_OK
+    if _CUDA_OK:
+        return
     if not torch.cuda.is_available():
         raise RuntimeError("paper_2405_02520_b200 needs a CUDA device (there is no CPU fallback)")
+    _CUDA_OK = True
 
 
 def torch_dtype(np_dtype):
@@ -80,11 +90,18 @@ def to_host(t: torch.Tensor) -> np.ndarray:
 
 
 def torch_current_device() -> int:
-    return torch.cuda.current_device()
+    return torch._C._cuda_getDevice()
 
 
 def stream_ptr():
-    return torch.cuda.current_stream().cuda_stream
+    """The raw cudaStream_t of torch's current stream on the current device
+    (the direct binding: torch.cuda.current_stream() builds a Stream object
+    and re-checks availability on every call)."""
+    global _INIT
+    if not _INIT:
+        torch.cuda.init()  # the raw bindings below assume an initialised CUDA state
+        _INIT = True
+    return torch._C._cuda_getCurrentRawStream(torch._C._cuda_getDevice())
 
 
 def ptr(t) -> int | None:

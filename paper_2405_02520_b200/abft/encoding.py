@@ -126,7 +126,7 @@ def make_encoding(kind, length: int) -> EncodingVector:
     if length < 1:
         raise ValueError("encoding length must be >= 1")
     _device.require_cuda()
-    return _make(kind, int(length), torch.cuda.current_device())
+    return _make(kind, int(length), _device.torch_current_device())
 
 
 def jou_variant_input(x):
