@@ -330,13 +330,18 @@ PASS_CANDIDATES = {
                (16, (16, 8), 16, 2, 4), (16, (16, 8), 8, 3, 4)),
         8: _pc((16, (16, 16), 16, 1, 0), (16, (16, 16), 16, 2, 1), (16, (16, 16), 8, 3, 1),
                (16, (16, 16), 8, 2, 0), (16, (16, 16), 16, 2, 2), (16, (16, 16), 8, 3, 2),
-               (16, (16, 16), 16, 2, 3), (16, (16, 16), 8, 3, 3), (16, (16, 16), 16, 2, 4)),
+               (16, (16, 16), 16, 2, 3), (16, (16, 16), 8, 3, 3), (16, (16, 16), 16, 2, 4),
+               (32, (32, 8), 16, 2, 3), (32, (32, 8), 8, 3, 3), (32, (32, 8), 16, 2, 2)),
         9: _pc((16, (16, 16, 2), 16, 1, 0), (16, (16, 16, 2), 8, 2, 1), (16, (16, 16, 2), 4, 3, 1),
                (16, (16, 16, 2), 8, 2, 0), (16, (16, 16, 2), 8, 2, 2), (16, (16, 16, 2), 16, 1, 2),
-               (16, (16, 16, 2), 16, 1, 3), (16, (16, 16, 2), 8, 2, 3)),
+               (16, (16, 16, 2), 16, 1, 3), (16, (16, 16, 2), 8, 2, 3),
+               (32, (32, 16), 8, 2, 3), (32, (32, 16), 16, 1, 3), (32, (32, 16), 8, 2, 2),
+               (32, (32, 16), 4, 3, 2)),
         10: _pc((16, (16, 16, 4), 8, 1, 0), (16, (16, 16, 4), 4, 2, 1), (16, (16, 16, 4), 4, 3, 0),
                 (32, (32, 32), 8, 1, 1), (16, (16, 16, 4), 8, 1, 1), (16, (16, 16, 4), 8, 1, 2),
-                (16, (16, 16, 4), 4, 2, 2), (16, (16, 16, 4), 8, 1, 3), (16, (16, 16, 4), 4, 2, 3)),
+                (16, (16, 16, 4), 4, 2, 2), (16, (16, 16, 4), 8, 1, 3), (16, (16, 16, 4), 4, 2, 3),
+                (32, (32, 32), 8, 1, 3), (32, (32, 32), 4, 2, 2), (32, (32, 32), 4, 2, 3),
+                (32, (32, 32), 8, 1, 2)),
         11: _pc((16, (16, 16, 8), 4, 1, 0), (16, (16, 16, 8), 4, 2, 1), (16, (16, 16, 8), 2, 3, 1),
                 (32, (32, 16, 4), 4, 1, 1), (16, (16, 16, 8), 4, 1, 2), (16, (16, 16, 8), 2, 2, 2),
                 (16, (16, 16, 8), 4, 1, 3), (16, (16, 16, 8), 2, 2, 3)),
