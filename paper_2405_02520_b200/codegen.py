@@ -374,9 +374,11 @@ PASS_CANDIDATES = {
 # (first, middle, last) variant per log2 L; missing -> (0, 0, 0).
 # Source: tools/tune_pass.py on a B200, ABFT on, 1 GiB (profiles/tune_pass_r01.json);
 # round 2: fp64 L = 512 last pass -> E = 16 (16, 16, 2), U = 4, bulk rows
-# (fp64 2^25 transform 1.462 -> 1.377 ms per GiB, profiles/tune_pass_fp64_25.json).
+# (fp64 2^25 transform 1.462 -> 1.377 ms per GiB, profiles/tune_pass_fp64_25.json);
+# fp32 L = 256 / 512 / 1024 -> E = 32 tiles (fp32 2^17 1.135 -> 0.961 ms, 2^19
+# 1.206 -> 1.094 ms per GiB, profiles/tune_pass_fp32_16.json).
 PASS_CHOICE = {
-    "fp32": {6: (6, 2, 4), 7: (9, 9, 5), 8: (6, 6, 5), 9: (6, 0, 7), 10: (7, 0, 6), 11: (6, 0, 6)},
+    "fp32": {6: (6, 2, 4), 7: (9, 9, 5), 8: (9, 6, 10), 9: (9, 0, 10), 10: (7, 0, 9), 11: (6, 0, 6)},
     "fp64": {6: (5, 5, 0), 7: (8, 8, 8), 8: (6, 6, 6), 9: (2, 0, 8), 10: (6, 0, 6), 11: (0, 0, 3)},
 }
 
