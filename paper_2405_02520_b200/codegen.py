@@ -327,7 +327,9 @@ PASS_CANDIDATES = {
         7: _pc((16, (16, 8), 16, 1, 0), (16, (16, 8), 16, 2, 1), (16, (16, 8), 8, 3, 1),
                (8, (8, 8, 2), 16, 2, 1), (16, (16, 8), 16, 2, 2), (16, (16, 8), 8, 3, 2),
                (16, (16, 8), 16, 2, 3), (16, (16, 8), 8, 3, 3), (16, (16, 8), 32, 1, 3),
-               (16, (16, 8), 16, 2, 4), (16, (16, 8), 8, 3, 4)),
+               (16, (16, 8), 16, 2, 4), (16, (16, 8), 8, 3, 4),
+               (32, (32, 4), 16, 3, 3), (32, (32, 4), 32, 2, 3), (32, (32, 4), 16, 3, 2),
+               (32, (32, 4), 32, 2, 4)),
         8: _pc((16, (16, 16), 16, 1, 0), (16, (16, 16), 16, 2, 1), (16, (16, 16), 8, 3, 1),
                (16, (16, 16), 8, 2, 0), (16, (16, 16), 16, 2, 2), (16, (16, 16), 8, 3, 2),
                (16, (16, 16), 16, 2, 3), (16, (16, 16), 8, 3, 3), (16, (16, 16), 16, 2, 4),
