@@ -73,20 +73,23 @@ SINGLE_CANDIDATES = {
                    (16, (16, 16, 8), 256, 2, 4), (32, (32, 32, 2), 128, 3, 0), (32, (32, 16, 4), 128, 3, 0),
                    (32, (32, 16, 4), 128, 2, 6), (32, (32, 32, 2), 128, 2, 6), (16, (16, 16, 8), 256, 2, 6),
                    (32, (32, 16, 4), 128, 3, 2), (32, (32, 16, 4), 128, 3, 4), (32, (32, 16, 4), 128, 2, 2),
-                   (32, (32, 16, 4), 128, 2, 4)),
+                   (32, (32, 16, 4), 128, 2, 4),
+                   (32, (16, 16, 8), 128, 3, 4), (32, (8, 16, 16), 128, 3, 4), (32, (32, 8, 8), 128, 3, 4)),
         12: _cands((16, (16, 16, 16), 256, 2, 0), (16, (16, 16, 16), 256, 3, 0),
                    (8, (8, 8, 8, 8), 512, 2, 0), (16, (16, 16, 16), 512, 1, 0),
                    (16, (16, 16, 16), 256, 3, 2), (16, (16, 16, 16), 256, 2, 2),
                    (16, (16, 16, 16), 256, 2, 4), (32, (32, 32, 4), 128, 3, 0), (32, (32, 16, 8), 128, 3, 0),
                    (16, (16, 16, 16), 256, 2, 6), (32, (32, 16, 8), 128, 2, 6),
-                   (32, (32, 16, 8), 128, 3, 4), (32, (32, 16, 8), 128, 2, 4), (32, (32, 16, 8), 128, 3, 2)),
+                   (32, (32, 16, 8), 128, 3, 4), (32, (32, 16, 8), 128, 2, 4), (32, (32, 16, 8), 128, 3, 2),
+                   (32, (16, 16, 16), 128, 3, 4), (32, (16, 32, 8), 128, 3, 4), (32, (8, 32, 16), 128, 3, 4)),
         13: _cands((16, (16, 16, 16, 2), 512, 2, 0), (32, (32, 16, 16), 256, 1, 0),
                    (16, (16, 16, 16, 2), 512, 1, 0), (8, (8, 8, 8, 8, 2), 1024, 1, 0),
                    (16, (16, 16, 16, 2), 512, 2, 2), (16, (16, 16, 16, 2), 512, 1, 2),
                    (16, (16, 16, 16, 2), 512, 2, 1), (16, (16, 16, 16, 2), 512, 2, 4),
                    (16, (16, 16, 16, 2), 512, 1, 4), (16, (16, 16, 16, 2), 512, 1, 6),
                    (32, (32, 16, 16), 256, 1, 6), (32, (32, 16, 16), 256, 1, 4),
-                   (32, (32, 16, 16), 256, 1, 2)),
+                   (32, (32, 16, 16), 256, 1, 2),
+                   (32, (16, 16, 32), 256, 1, 4), (32, (16, 32, 16), 256, 1, 4), (32, (32, 32, 8), 256, 1, 4)),
     },
     "fp64": {
         1: _cands((2, (2,), 256, 1, 1), (2, (2,), 256, 1, 0), (2, (2,), 256, 1, 3)),
@@ -378,9 +381,11 @@ PASS_CANDIDATES = {
 # round 2: fp64 L = 512 last pass -> E = 16 (16, 16, 2), U = 4, bulk rows
 # (fp64 2^25 transform 1.462 -> 1.377 ms per GiB, profiles/tune_pass_fp64_25.json);
 # fp32 L = 256 / 512 / 1024 -> E = 32 tiles (fp32 2^17 1.135 -> 0.961 ms, 2^19
-# 1.206 -> 1.094 ms per GiB, profiles/tune_pass_fp32_16.json).
+# 1.206 -> 1.094 ms per GiB, profiles/tune_pass_fp32_16.json); fp32 L = 128
+# middle / last -> E = 32 (2^21 -3 %, 2^14 -3 %, profiles/tune_pass_fp32_14.json,
+# tune_pass_fp32_21.json), L = 256 middle -> TMA prefetch PF 4 (2^24 -1.5 %).
 PASS_CHOICE = {
-    "fp32": {6: (6, 2, 4), 7: (9, 9, 5), 8: (9, 6, 10), 9: (9, 0, 10), 10: (7, 0, 9), 11: (6, 0, 6)},
+    "fp32": {6: (6, 2, 4), 7: (9, 12, 11), 8: (9, 9, 10), 9: (9, 0, 10), 10: (7, 0, 9), 11: (6, 0, 6)},
     "fp64": {6: (5, 5, 0), 7: (8, 8, 8), 8: (6, 6, 6), 9: (2, 0, 8), 10: (6, 0, 6), 11: (0, 0, 3)},
 }
 
