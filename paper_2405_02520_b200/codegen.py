@@ -355,14 +355,18 @@ PASS_CANDIDATES = {
         1: _pc((2, (2,), 8, 1, 0)), 2: _pc((4, (4,), 8, 1, 0)), 3: _pc((8, (8,), 8, 1, 0)),
         4: _pc((16, (16,), 8, 1, 0)), 5: _pc((8, (8, 4), 8, 1, 0)),
         6: _pc((8, (8, 8), 8, 1, 0), (8, (8, 8), 16, 2, 3), (8, (8, 8), 8, 3, 3), (8, (8, 8), 16, 2, 2),
-               (8, (8, 8), 8, 3, 2), (8, (8, 8), 16, 2, 4)),
+               (8, (8, 8), 8, 3, 2), (8, (8, 8), 16, 2, 4),
+               (16, (16, 4), 16, 2, 3), (16, (16, 4), 8, 3, 3), (16, (16, 4), 16, 2, 4)),
         7: _pc((16, (16, 8), 8, 1, 0), (16, (16, 8), 8, 2, 1), (16, (16, 8), 4, 3, 1),
                (8, (8, 8, 2), 8, 2, 1), (16, (16, 8), 8, 2, 2), (16, (16, 8), 4, 3, 2),
                (16, (16, 8), 8, 2, 3), (16, (16, 8), 4, 3, 3), (16, (16, 8), 16, 1, 3),
-               (16, (16, 8), 16, 1, 4), (16, (16, 8), 8, 2, 4)),
+               (16, (16, 8), 16, 1, 4), (16, (16, 8), 8, 2, 4),
+               (32, (32, 4), 8, 2, 3), (32, (32, 4), 16, 1, 3), (32, (32, 4), 8, 2, 2)),
         8: _pc((16, (16, 16), 8, 1, 0), (16, (16, 16), 8, 2, 1), (16, (16, 16), 4, 2, 1),
                (8, (8, 8, 4), 8, 2, 1), (16, (16, 16), 8, 2, 2), (8, (8, 8, 4), 8, 2, 2),
-               (16, (16, 16), 8, 2, 3), (8, (8, 8, 4), 8, 2, 3), (16, (16, 16), 8, 2, 4)),
+               (16, (16, 16), 8, 2, 3), (8, (8, 8, 4), 8, 2, 3), (16, (16, 16), 8, 2, 4),
+               (32, (32, 8), 8, 1, 3), (32, (32, 8), 4, 2, 3), (32, (32, 8), 8, 1, 2),
+               (32, (32, 8), 4, 2, 2)),
         9: _pc((8, (8, 8, 8), 8, 1, 0), (8, (8, 8, 8), 4, 2, 1), (16, (16, 16, 2), 4, 2, 1),
                (8, (8, 8, 8), 8, 1, 1), (8, (8, 8, 8), 8, 1, 2), (8, (8, 8, 8), 4, 2, 2),
                (8, (8, 8, 8), 8, 1, 3), (8, (8, 8, 8), 4, 2, 3),
