@@ -387,10 +387,12 @@ PASS_CANDIDATES = {
 # fp32 L = 256 / 512 / 1024 -> E = 32 tiles (fp32 2^17 1.135 -> 0.961 ms, 2^19
 # 1.206 -> 1.094 ms per GiB, profiles/tune_pass_fp32_16.json); fp32 L = 128
 # middle / last -> E = 32 (2^21 -3 %, 2^14 -3 %, profiles/tune_pass_fp32_14.json,
-# tune_pass_fp32_21.json), L = 256 middle -> TMA prefetch PF 4 (2^24 -1.5 %).
+# tune_pass_fp32_21.json), L = 256 middle -> TMA prefetch PF 4 (2^24 -1.5 %);
+# fp64 L = 256 last -> E = 32 (2^16 -2.9 %, 2^22 -1.0 %, tune_pass_fp64_16b.json /
+# tune_pass_fp64_20.json: every other fp64 choice stayed the best).
 PASS_CHOICE = {
     "fp32": {6: (6, 2, 4), 7: (9, 12, 11), 8: (9, 9, 10), 9: (9, 0, 10), 10: (7, 0, 9), 11: (6, 0, 6)},
-    "fp64": {6: (5, 5, 0), 7: (8, 8, 8), 8: (6, 6, 6), 9: (2, 0, 8), 10: (6, 0, 6), 11: (0, 0, 3)},
+    "fp64": {6: (5, 5, 0), 7: (8, 8, 8), 8: (6, 6, 11), 9: (2, 0, 8), 10: (6, 0, 6), 11: (0, 0, 3)},
 }
 
 
