@@ -117,7 +117,7 @@ constexpr size_t kBlockHead = kFixOff + kFixCap * sizeof(FixRes);
 static_assert(sizeof(Counters) <= kFixOff && kBlockHead % 64 == 0, "detection block layout");
 
 // [prec][logn][variant] -> entry, plus the tuned default and a runtime override
-constexpr int kMaxVariants = 16;
+constexpr int kMaxVariants = 32;
 struct SingleIndex {
     const SingleEntry* e[2][14][kMaxVariants] = {};
     int count[2][14] = {};
@@ -375,6 +375,7 @@ int launch_single_t(tfft_plan* p, const Launch& L, cudaStream_t st) {
         if (rc2) return rc2;
     }
     long long grid = std::min<long long>(tiles, (long long)nb * p->num_sms);
+    if (e->stage & 64) grid = std::max<long long>(2, ((long long)nb * p->num_sms) & ~1LL);  // whole 2-CTA clusters
     if (grid < 1) grid = 1;
     void* args[] = {&a};
     CU((tfft::note_launch(), cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(e->threads), args, e->smem, st)));
