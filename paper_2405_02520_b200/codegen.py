@@ -89,11 +89,7 @@ SINGLE_CANDIDATES = {
                    (16, (16, 16, 16, 2), 512, 1, 4), (16, (16, 16, 16, 2), 512, 1, 6),
                    (32, (32, 16, 16), 256, 1, 6), (32, (32, 16, 16), 256, 1, 4),
                    (32, (32, 16, 16), 256, 1, 2),
-                   (32, (16, 16, 32), 256, 1, 4), (32, (16, 32, 16), 256, 1, 4), (32, (32, 32, 8), 256, 1, 4),
-                   # 2-CTA cluster kernel (stage code 64): radices of the N/2 half
-                   (16, (16, 16, 16), 256, 2, 64), (16, (16, 16, 16), 256, 1, 64),
-                   (16, (16, 16, 16), 256, 1, 64 + 128), (16, (16, 16, 16), 256, 1, 64 + 256),
-                   (16, (16, 16, 16), 256, 1, 64 + 128 + 256)),
+                   (32, (16, 16, 32), 256, 1, 4), (32, (16, 32, 16), 256, 1, 4), (32, (32, 32, 8), 256, 1, 4)),
     },
     "fp64": {
         1: _cands((2, (2,), 256, 1, 1), (2, (2,), 256, 1, 0), (2, (2,), 256, 1, 3)),
@@ -239,12 +235,10 @@ def single_configs(all_candidates=True):
                     continue
                 n = 1 << logn
                 e, radices = c["e"], c["radices"]
-                cl = bool(c["stage"] & 64)  # 2-CTA cluster kernel (cluster.cuh): radices of the half
-                nh = n // 2 if cl else n
-                assert math.prod(radices) == nh and all(e % r == 0 for r in radices), (prec, logn, c)
-                tps = nh // e
+                assert math.prod(radices) == n and all(e % r == 0 for r in radices), (prec, logn, c)
+                tps = n // e
                 threads = max(c["threads"], tps)
-                ps, _ = choose_padding(nh, e, radices, prec)
+                ps, _ = choose_padding(n, e, radices, prec)
                 s = threads // tps
                 ex = (n + (n >> ps) + 1 if ps else n) if len(radices) > 1 else 0
                 ld = c["stage"] & 7  # load strategy (| 8: e^T W row from smem for short signals too)
@@ -258,8 +252,6 @@ def single_configs(all_candidates=True):
                 red = 10 * (threads // 32 + 1) + (10 * threads + 10 * s if tps >= 64 else 0)
                 regions = 2 if ld == 6 else 1  # ping-pong exchange regions
                 smem = (ib + regions * s * max(ex, st)) * ELEM_BYTES[prec] + red * (ELEM_BYTES[prec] // 2)
-                if cl:  # whole signal (multicast) + half exchange slice + partner's output quarter
-                    smem = (n + (nh + (nh >> ps) + 1 if ps else nh) + n // 4) * ELEM_BYTES[prec] + 64
                 out.append(dict(prec=prec, logn=logn, n=n, e=e, radices=radices, threads=threads,
                                 ps=ps, smem=smem, tps=tps, minb=c["minb"], stage=c["stage"],
                                 variant=vi, chosen=vi == chosen))
@@ -271,7 +263,6 @@ def _emit_single(prec, cfgs, part, table=False):
     lines = [
         "// GENERATED by paper_2405_02520_b200/codegen.py — do not edit.",
         '#include "fix.cuh"',
-        '#include "cluster.cuh"',
         '#include "registry.h"',
         "namespace tfft {",
     ]
@@ -283,8 +274,7 @@ def _emit_single(prec, cfgs, part, table=False):
             if abft >= 2 and not c["chosen"]:
                 fns.append("nullptr")  # table / thread-level checks only on the chosen config
                 continue
-            kern = "fft_cluster_kernel" if c["stage"] & 64 else "fft_single_kernel"
-            fns.append(f"(const void*)&{kern}<{t}, {c['n']}, {c['e']}, {c['ps']}, "
+            fns.append(f"(const void*)&fft_single_kernel<{t}, {c['n']}, {c['e']}, {c['ps']}, "
                        f"{abft}, {c['threads']}, {c['minb']}, {c['stage']}, RList<{rl}>>")
         fix = "nullptr, 0, 0"
         if c["chosen"]:  # device-side correction with the same engine config (fix.cuh)

@@ -375,7 +375,6 @@ int launch_single_t(tfft_plan* p, const Launch& L, cudaStream_t st) {
         if (rc2) return rc2;
     }
     long long grid = std::min<long long>(tiles, (long long)nb * p->num_sms);
-    if (e->stage & 64) grid = std::max<long long>(2, ((long long)nb * p->num_sms) & ~1LL);  // whole 2-CTA clusters
     if (grid < 1) grid = 1;
     void* args[] = {&a};
     CU((tfft::note_launch(), cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(e->threads), args, e->smem, st)));
