@@ -81,7 +81,8 @@ SINGLE_CANDIDATES = {
                    (16, (16, 16, 16), 256, 2, 4), (32, (32, 32, 4), 128, 3, 0), (32, (32, 16, 8), 128, 3, 0),
                    (16, (16, 16, 16), 256, 2, 6), (32, (32, 16, 8), 128, 2, 6),
                    (32, (32, 16, 8), 128, 3, 4), (32, (32, 16, 8), 128, 2, 4), (32, (32, 16, 8), 128, 3, 2),
-                   (32, (16, 16, 16), 128, 3, 4), (32, (16, 32, 8), 128, 3, 4), (32, (8, 32, 16), 128, 3, 4)),
+                   (32, (16, 16, 16), 128, 3, 4), (32, (16, 32, 8), 128, 3, 4), (32, (8, 32, 16), 128, 3, 4),
+                   (32, (32, 16, 8), 128, 3, 4 + 32), (32, (32, 16, 8), 128, 2, 4 + 32)),
         13: _cands((16, (16, 16, 16, 2), 512, 2, 0), (32, (32, 16, 16), 256, 1, 0),
                    (16, (16, 16, 16, 2), 512, 1, 0), (8, (8, 8, 8, 8, 2), 1024, 1, 0),
                    (16, (16, 16, 16, 2), 512, 2, 2), (16, (16, 16, 16, 2), 512, 1, 2),
@@ -89,7 +90,9 @@ SINGLE_CANDIDATES = {
                    (16, (16, 16, 16, 2), 512, 1, 4), (16, (16, 16, 16, 2), 512, 1, 6),
                    (32, (32, 16, 16), 256, 1, 6), (32, (32, 16, 16), 256, 1, 4),
                    (32, (32, 16, 16), 256, 1, 2),
-                   (32, (16, 16, 32), 256, 1, 4), (32, (16, 32, 16), 256, 1, 4), (32, (32, 32, 8), 256, 1, 4)),
+                   (32, (16, 16, 32), 256, 1, 4), (32, (16, 32, 16), 256, 1, 4), (32, (32, 32, 8), 256, 1, 4),
+                   (32, (32, 16, 16), 256, 1, 4 + 32), (32, (32, 16, 16), 256, 1, 2 + 32),
+                   (32, (32, 32, 8), 256, 1, 4 + 32), (16, (16, 16, 16, 2), 512, 1, 4 + 32)),
     },
     "fp64": {
         1: _cands((2, (2,), 256, 1, 1), (2, (2,), 256, 1, 0), (2, (2,), 256, 1, 3)),
@@ -117,11 +120,13 @@ SINGLE_CANDIDATES = {
         11: _cands((16, (16, 16, 8), 256, 1, 0), (16, (16, 16, 8), 256, 2, 0),
                    (8, (8, 8, 8, 4), 256, 2, 0), (16, (16, 16, 8), 256, 2, 2),
                    (8, (8, 8, 8, 4), 256, 2, 4), (16, (16, 16, 8), 128, 3, 0), (16, (16, 16, 8), 128, 2, 0),
-                   (16, (16, 16, 8), 256, 1, 6), (16, (16, 16, 8), 128, 1, 6)),
+                   (16, (16, 16, 8), 256, 1, 6), (16, (16, 16, 8), 128, 1, 6),
+                   (16, (16, 16, 8), 128, 2, 32), (16, (16, 16, 8), 128, 3, 32)),
         12: _cands((16, (16, 16, 16), 256, 1, 0), (16, (16, 16, 16), 512, 1, 0),
                    (8, (8, 8, 8, 8), 512, 1, 0), (16, (16, 16, 16), 256, 1, 2),
                    (16, (16, 16, 16), 256, 1, 4), (8, (8, 8, 8, 8), 512, 1, 4),
-                   (8, (8, 8, 8, 8), 512, 2, 4), (16, (16, 16, 16), 256, 1, 6)),
+                   (8, (8, 8, 8, 8), 512, 2, 4), (16, (16, 16, 16), 256, 1, 6),
+                   (16, (16, 16, 16), 256, 1, 4 + 32)),
         13: _cands((16, (16, 16, 16, 2), 512, 1, 0), (8, (8, 8, 8, 8, 2), 1024, 1, 0),
                    (16, (16, 16, 16, 2), 512, 1, 4), (8, (8, 8, 8, 8, 2), 1024, 1, 4)),
     },
@@ -140,8 +145,8 @@ SINGLE_CANDIDATES = {
 # the in-place TMA prefetch (0.473 -> 0.423 / 0.444 -> 0.424 ms,
 # profiles/tune_r02f_fp32.json).
 SINGLE_CHOICE = {
-    "fp32": {1: 1, 2: 1, 3: 4, 4: 5, 5: 14, 6: 5, 7: 0, 8: 4, 9: 7, 10: 9, 11: 13, 12: 11, 13: 11},
-    "fp64": {1: 1, 2: 2, 3: 3, 4: 7, 5: 5, 6: 4, 7: 0, 8: 4, 9: 6, 10: 4, 11: 5, 12: 4, 13: 2},
+    "fp32": {1: 1, 2: 1, 3: 4, 4: 5, 5: 14, 6: 5, 7: 0, 8: 4, 9: 7, 10: 9, 11: 13, 12: 11, 13: 16},
+    "fp64": {1: 1, 2: 2, 3: 3, 4: 7, 5: 5, 6: 4, 7: 0, 8: 4, 9: 6, 10: 4, 11: 5, 12: 8, 13: 2},
 }
 ELEM_BYTES = {"fp32": 8, "fp64": 16}
 CTYPE = {"fp32": "float", "fp64": "double"}
@@ -241,7 +246,7 @@ def single_configs(all_candidates=True):
                 ps, _ = choose_padding(n, e, radices, prec)
                 s = threads // tps
                 ex = (n + (n >> ps) + 1 if ps else n) if len(radices) > 1 else 0
-                ld = c["stage"] & 7  # load strategy (| 8: e^T W row from smem for short signals too)
+                ld = c["stage"] & 7  # load strategy (| 8 / | 32: e^T W row from static / dynamic smem)
                 st = n + 1 if ld in (1, 3) else (n if ld == 4 else 0)
                 ib = s * n if ld in (2, 3, 6) else 0  # TMA prefetch buffer
                 if ld == 5:  # per-signal rows into padded slots
@@ -252,6 +257,8 @@ def single_configs(all_candidates=True):
                 red = 10 * (threads // 32 + 1) + (10 * threads + 10 * s if tps >= 64 else 0)
                 regions = 2 if ld == 6 else 1  # ping-pong exchange regions
                 smem = (ib + regions * s * max(ex, st)) * ELEM_BYTES[prec] + red * (ELEM_BYTES[prec] // 2)
+                if c["stage"] & 32:  # e^T W row behind the (16-byte rounded) ABFT scratch
+                    smem += ((red + 3) // 4 * 4 - red) * (ELEM_BYTES[prec] // 2) + n * ELEM_BYTES[prec]
                 out.append(dict(prec=prec, logn=logn, n=n, e=e, radices=radices, threads=threads,
                                 ps=ps, smem=smem, tps=tps, minb=c["minb"], stage=c["stage"],
                                 variant=vi, chosen=vi == chosen))

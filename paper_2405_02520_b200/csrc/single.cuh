@@ -303,6 +303,10 @@ fft_single_kernel(const __grid_constant__ SingleArgs<T> a) {
     constexpr int STAGE = STAGE_CODE & 7;
     constexpr bool EW_SM_ALL = (STAGE_CODE & 8) != 0;
     constexpr bool SHFL = (STAGE_CODE & 16) != 0;  // warp-shuffle transpose stage (E = TPS = radix)
+    // | 32: the e^T W row in DYNAMIC shared memory behind the ABFT scratch,
+    // for any N (the static copy below is capped at 16 KB); for kernels whose
+    // occupancy registers, not shared memory, set (fp32 N = 4096 / 8192)
+    constexpr bool EWB = (STAGE_CODE & 32) != 0;
     using Eng = Engine<T, N, E, Radices>;
     constexpr int TPS = N / E;
     constexpr int S = THREADS / TPS;  // signals per CTA
@@ -343,6 +347,8 @@ fft_single_kernel(const __grid_constant__ SingleArgs<T> a) {
     C<T>* ib = reinterpret_cast<C<T>*>(smem_raw);  // prefetch buffer (PF)
     C<T>* sm_all = ib + (PF ? S * SLP : 0);
     T* red = reinterpret_cast<T*>(sm_all + (PP ? 2 : 1) * S * SL);  // 5 partial sums per warp
+    // ABFT scratch size in T (codegen.single_configs `red`), rounded to 16 bytes
+    constexpr int RED_T = (10 * (THREADS / 32 + 1) + (TPS >= 64 ? 10 * THREADS + 10 * S : 0) + 3) / 4 * 4;
     __shared__ typename KeyT<T>::type cta_max;
     __shared__ unsigned long long in_bar;
 
@@ -487,8 +493,10 @@ fft_single_kernel(const __grid_constant__ SingleArgs<T> a) {
     // per-tile reads are then LDS instead of L1-hit LDGs (fp32 N = 2048:
     // 0.512 -> 0.491 ms; at 32 KB the lost occupancy costs more than it saves)
     // (not with the ping-pong regions, whose dynamic smem already sets the occupancy)
-    constexpr bool EWS = TFFT_EW_SMEM && TB && (TPS >= 64 || EW_SM_ALL) && N * (int)sizeof(C<T>) <= 16384 && !PP;
-    __shared__ C<T> etw_sm[EWS ? N : 1];
+    constexpr bool EWS = TFFT_EW_SMEM && TB &&
+                         (EWB || ((TPS >= 64 || EW_SM_ALL) && N * (int)sizeof(C<T>) <= 16384 && !PP));
+    __shared__ C<T> etw_st[EWS && !EWB ? N : 1];
+    C<T>* const etw_sm = EWB ? reinterpret_cast<C<T>*>(red + RED_T) : etw_st;
     if constexpr (EWS) {
         for (int i = threadIdx.x; i < N; i += THREADS) etw_sm[i] = a.etw[i];
         __syncthreads();
