@@ -33,6 +33,9 @@ enum { AT_NONE = 0, AT_INPUT = 1, AT_PRESCALE = 2, AT_OUTPUT = 3 };
 #ifndef TFFT_DEFER_MIN
 #define TFFT_DEFER_MIN 128  // signals of >= this many threads use the smem partial pipeline
 #endif
+#ifndef TFFT_ONE_LOOP_ALL
+#define TFFT_ONE_LOOP_ALL 0  // experiment builds: every config with the single runtime tile loop
+#endif
 #ifndef TFFT_EW_SMEM
 #define TFFT_EW_SMEM 1
 #endif
@@ -294,6 +297,15 @@ __device__ __forceinline__ void stage_out(C<T>* __restrict__ dst, long long vali
     }
 }
 
+template <bool B>
+struct BoolC {
+    static constexpr bool value = B;
+};
+template <int I>
+struct IntC {
+    static constexpr int value = I;
+};
+
 template <class T, int N, int E, int PS, int ABFT, int THREADS, int MINB, int STAGE_CODE, class Radices>
 __global__ void __launch_bounds__(THREADS, MINB)
 fft_single_kernel(const __grid_constant__ SingleArgs<T> a) {
@@ -307,6 +319,9 @@ fft_single_kernel(const __grid_constant__ SingleArgs<T> a) {
     // for any N (the static copy below is capped at 16 KB); for kernels whose
     // occupancy registers, not shared memory, set (fp32 N = 4096 / 8192)
     constexpr bool EWB = (STAGE_CODE & 32) != 0;
+    // | 64: ONE tile loop with the direction and the fault injection decided
+    // at run time (fewer registers: the occupancy of some short-signal configs)
+    constexpr bool ONE_LOOP = (STAGE_CODE & 64) != 0 || TFFT_ONE_LOOP_ALL;
     using Eng = Engine<T, N, E, Radices>;
     constexpr int TPS = N / E;
     constexpr int S = THREADS / TPS;  // signals per CTA
@@ -501,6 +516,14 @@ fft_single_kernel(const __grid_constant__ SingleArgs<T> a) {
         for (int i = threadIdx.x; i < N; i += THREADS) etw_sm[i] = a.etw[i];
         __syncthreads();
     }
+    // the persistent tile loop, instantiated for the fault-free forward and
+    // inverse transforms and once for fault injection (runtime direction):
+    // the inverse's re/im swaps and the injection selects would otherwise cost
+    // predicated moves on every element of every tile
+    auto tile_loop = [&](auto dir_c, auto flt_c) {
+    constexpr int DIR = decltype(dir_c)::value;  // 0 forward, 1 inverse, 2 a.inverse
+    constexpr bool FLT = decltype(flt_c)::value;
+    const bool INV = DIR == 2 ? a.inverse != 0 : DIR == 1;
     unsigned iter = 0;
     for (long long tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++iter) {
         const long long b = tile * S + sl;
@@ -609,13 +632,13 @@ fft_single_kernel(const __grid_constant__ SingleArgs<T> a) {
         }
         int fw = a.f_where, fc = a.f_comp, fb = a.f_bit;
         long long fs = a.f_signal, fe = a.f_elem;
-        if (a.f_table != nullptr && live) {  // batched campaign (never on the product path)
+        if (FLT && a.f_table != nullptr && live) {  // batched campaign (never on the product path)
             const long long g = a.sig_base + b, r = g / a.f_div;
             const FaultRec fr = a.f_table[r];
             fw = fr.where; fc = fr.comp; fb = fr.bit;
             fs = r * a.f_div + fr.signal; fe = fr.pos;
         }
-        const bool fault_here = fw != AT_NONE && live && (a.sig_base + b) == fs && (int)(fe % TPS) == t;
+        const bool fault_here = FLT && fw != AT_NONE && live && (a.sig_base + b) == fs && (int)(fe % TPS) == t;
         const int fm = (int)(fe / TPS);
         if (fault_here && fw == AT_INPUT) {
 #pragma unroll
@@ -623,7 +646,7 @@ fft_single_kernel(const __grid_constant__ SingleArgs<T> a) {
         }
 
         // ---- transform (inverse = swap(FFT(swap(x))) — conjugate symmetry)
-        if (a.inverse) {
+        if (INV) {
 #pragma unroll
             for (int m = 0; m < E; ++m) v[m] = swapri<T>(v[m]);
         }
@@ -660,7 +683,7 @@ fft_single_kernel(const __grid_constant__ SingleArgs<T> a) {
             if constexpr (ABFT == ABFT_THREAD) Eng::run(v, mem, t, a.tw, tchk);
             else Eng::run(v, mem, t, a.tw);
         }
-        if (a.inverse) {
+        if (INV) {
 #pragma unroll
             for (int m = 0; m < E; ++m) v[m] = swapri<T>(v[m]);
         }
@@ -810,6 +833,10 @@ fft_single_kernel(const __grid_constant__ SingleArgs<T> a) {
             }
         }
     }
+    };
+    if (ONE_LOOP || a.f_where != AT_NONE || a.f_table != nullptr) tile_loop(IntC<2>{}, BoolC<true>{});
+    else if (a.inverse) tile_loop(IntC<1>{}, BoolC<false>{});
+    else tile_loop(IntC<0>{}, BoolC<false>{});
     if constexpr (DEFER1) {
         if (pend) {
             __syncthreads();
