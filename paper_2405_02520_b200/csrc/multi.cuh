@@ -291,6 +291,12 @@ fft_pass_kernel(const __grid_constant__ PassArgs<T> a) {
         if (threadIdx.x < U && blockIdx.x < total) cf_col_base(blockIdx.x, 0);
         __syncthreads();
     }
+    // the tile loop, instantiated per direction and once for fault injection
+    // (as in single.cuh): no per-element predicated swaps / injection selects
+    auto tile_loop = [&](auto dir_c, auto flt_c) {
+    constexpr int DIR = decltype(dir_c)::value;  // 0 forward, 1 inverse, 2 a.inverse
+    constexpr bool FLT = decltype(flt_c)::value;
+    const bool INV = DIR == 2 ? a.inverse != 0 : DIR == 1;
     unsigned it = 0;
     for (long long tix = blockIdx.x; tix < total; tix += gridDim.x, ++it) {
         C<T>* cur = (PF && (it & 1)) ? tile + BUFE : tile;
@@ -306,13 +312,13 @@ fft_pass_kernel(const __grid_constant__ PassArgs<T> a) {
         const long long obase = hi * a.out_hi + lo * a.out_lo;
         int fw = a.f_where, fc = a.f_comp, fb = a.f_bit, fi = a.f_idx;
         long long fs = a.f_signal, fu = a.f_unit;
-        if (a.f_table != nullptr) {  // batched campaign (never on the product path)
+        if (FLT && a.f_table != nullptr) {  // batched campaign (never on the product path)
             const long long g = a.sig_base + b, r = g / a.f_div;
             const FaultRec fr = a.f_table[r];
             fw = fr.where; fc = fr.comp; fb = fr.bit; fi = fr.idx;
             fs = r * a.f_div + fr.signal; fu = fr.pos;
         }
-        const bool fsig = fw != 0 && (a.sig_base + b) == fs && uu == fu && (fi % TPS) == t;
+        const bool fsig = FLT && fw != 0 && (a.sig_base + b) == fs && uu == fu && (fi % TPS) == t;
         const int fm = fi / TPS;
 
         // input-side ABFT row e^T W for this tile, requested before the tile
@@ -327,7 +333,7 @@ fft_pass_kernel(const __grid_constant__ PassArgs<T> a) {
             // one of them (m*) can lie within 1/256 rad of the pole; find it with
             // integer arithmetic and patch it after the addition formula
             const int N3 = 3 * cf_n, H = N3 / 2;
-            const int dk = (a.inverse ? -3 : 3) * (int)a.in_j;  // +-3 N / L per row
+            const int dk = (INV ? -3 : 3) * (int)a.in_j;  // +-3 N / L per row
             int kt = cf_kc[par * U + u] + dk * t;
             if (kt > H) kt -= N3;
             else if (kt <= -H) kt += N3;
@@ -439,7 +445,7 @@ fft_pass_kernel(const __grid_constant__ PassArgs<T> a) {
                 // x . etw = (A / 2)(S0 - i S1), S0 = sum x, S1 = sum x cot; A = 1 - w3^N
                 // = (1.5, +-sqrt(3)/2) for N = 1 / 2 (mod 3); inverse: also / N
                 const T hs = T(0.8660254037844386467637232) * ((a.n % 3 == 1) ? T(1) : T(-1));
-                const T g = a.inverse ? T(0.5) / T(a.n) : T(0.5);
+                const T g = INV ? T(0.5) / T(a.n) : T(0.5);
                 const C<T> u = mk<T>(fadd(ca[0].x, sa[0].y), fsub(ca[0].y, sa[0].x));
                 cin = cmul<T>(u, mk<T>(T(1.5) * g, hs * g));
             }
@@ -452,7 +458,7 @@ fft_pass_kernel(const __grid_constant__ PassArgs<T> a) {
             for (int m = 0; m < E; ++m) if (m == fm) flip_component<T>(v[m], fc, fb);
         }
 
-        if (a.inverse) {
+        if (INV) {
 #pragma unroll
             for (int m = 0; m < E; ++m) v[m] = swapri<T>(v[m]);
         }
@@ -474,7 +480,7 @@ fft_pass_kernel(const __grid_constant__ PassArgs<T> a) {
 #pragma unroll
             for (int m = 1; m < E; ++m) v[m] = cmul<T>(v[m], cmul<T>(base, st[m]));
         }
-        if (a.inverse) {
+        if (INV) {
 #pragma unroll
             for (int m = 0; m < E; ++m) v[m] = swapri<T>(v[m]);
         }
@@ -546,6 +552,10 @@ fft_pass_kernel(const __grid_constant__ PassArgs<T> a) {
             }
         }
     }
+    };
+    if (TFFT_ONE_LOOP_ALL || a.f_where != 0 || a.f_table != nullptr) tile_loop(IntC<2>{}, BoolC<true>{});
+    else if (a.inverse) tile_loop(IntC<1>{}, BoolC<false>{});
+    else tile_loop(IntC<0>{}, BoolC<false>{});
 }
 
 // Per-signal reduction of the tile partials and the detection decision.
