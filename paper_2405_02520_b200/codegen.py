@@ -145,14 +145,14 @@ SINGLE_CANDIDATES = {
 # the in-place TMA prefetch (0.473 -> 0.423 / 0.444 -> 0.424 ms,
 # profiles/tune_r02f_fp32.json).
 SINGLE_CHOICE = {
-    "fp32": {1: 1, 2: 1, 3: 4, 4: 5, 5: 14, 6: 5, 7: 0, 8: 4, 9: 7, 10: 9, 11: 13, 12: 11, 13: 16},
+    "fp32": {1: 1, 2: 1, 3: 4, 4: 5, 5: 17, 6: 8, 7: 0, 8: 4, 9: 7, 10: 9, 11: 18, 12: 13, 13: 16},
     "fp64": {1: 1, 2: 2, 3: 3, 4: 7, 5: 5, 6: 4, 7: 0, 8: 4, 9: 6, 10: 4, 11: 5, 12: 8, 13: 2},
 }
 # One-loop twins (stage code | 64, single.cuh ONE_LOOP) of the tuned configs:
 # the single kernel instantiates its tile loop per direction and once more for
 # fault injection; these sizes measured faster with ONE runtime loop (fewer
 # registers, more CTAs per SM) — A/B in profiles/ab_loop_r02.json.
-ONE_LOOP_SIZES = {"fp32": (4, 6, 7, 8), "fp64": (1, 5, 6, 13)}
+ONE_LOOP_SIZES = {"fp32": (4, 7, 8), "fp64": (1, 5, 6, 13)}
 for _p, _sizes in ONE_LOOP_SIZES.items():
     for _l in _sizes:
         _twin = dict(SINGLE_CANDIDATES[_p][_l][SINGLE_CHOICE[_p][_l]])

@@ -489,7 +489,7 @@ fft_pass_kernel(const __grid_constant__ PassArgs<T> a) {
             for (int m = 0; m < E; ++m) if (m == fm) flip_component<T>(v[m], fc, fb);
         }
         if constexpr (KIND == KIND_LAST) {
-            if (a.scale_inv) {
+            if (DIR != 0 && a.scale_inv) {  // the forward loop runs only unscaled
 #pragma unroll
                 for (int m = 0; m < E; ++m) v[m] = cscale<T>(v[m], a.scale);
             }
@@ -553,7 +553,8 @@ fft_pass_kernel(const __grid_constant__ PassArgs<T> a) {
         }
     }
     };
-    if (TFFT_ONE_LOOP_ALL || a.f_where != 0 || a.f_table != nullptr) tile_loop(IntC<2>{}, BoolC<true>{});
+    if (TFFT_ONE_LOOP_ALL || a.f_where != 0 || a.f_table != nullptr || (a.scale_inv && !a.inverse))
+        tile_loop(IntC<2>{}, BoolC<true>{});
     else if (a.inverse) tile_loop(IntC<1>{}, BoolC<false>{});
     else tile_loop(IntC<0>{}, BoolC<false>{});
 }

@@ -698,7 +698,7 @@ fft_single_kernel(const __grid_constant__ SingleArgs<T> a) {
 #pragma unroll
             for (int m = 0; m < E; ++m) if (m == fm) flip_component<T>(v[m], fc, fb);
         }
-        if (a.scale_inv) {
+        if (DIR != 0 && a.scale_inv) {  // the forward loop runs only unscaled
             const T s = T(1) / T(N);  // exact power of two
 #pragma unroll
             for (int m = 0; m < E; ++m) v[m] = cscale<T>(v[m], s);
@@ -834,7 +834,8 @@ fft_single_kernel(const __grid_constant__ SingleArgs<T> a) {
         }
     }
     };
-    if (ONE_LOOP || a.f_where != AT_NONE || a.f_table != nullptr) tile_loop(IntC<2>{}, BoolC<true>{});
+    if (ONE_LOOP || a.f_where != AT_NONE || a.f_table != nullptr || (a.scale_inv && !a.inverse))
+        tile_loop(IntC<2>{}, BoolC<true>{});
     else if (a.inverse) tile_loop(IntC<1>{}, BoolC<false>{});
     else tile_loop(IntC<0>{}, BoolC<false>{});
     if constexpr (DEFER1) {
