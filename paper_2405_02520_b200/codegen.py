@@ -146,7 +146,7 @@ SINGLE_CANDIDATES = {
 # profiles/tune_r02f_fp32.json).
 SINGLE_CHOICE = {
     "fp32": {1: 1, 2: 1, 3: 4, 4: 5, 5: 17, 6: 8, 7: 0, 8: 4, 9: 7, 10: 9, 11: 18, 12: 13, 13: 16},
-    "fp64": {1: 1, 2: 2, 3: 3, 4: 7, 5: 5, 6: 4, 7: 0, 8: 4, 9: 6, 10: 4, 11: 5, 12: 8, 13: 2},
+    "fp64": {1: 1, 2: 2, 3: 3, 4: 7, 5: 5, 6: 4, 7: 0, 8: 4, 9: 6, 10: 4, 11: 7, 12: 8, 13: 2},
 }
 # One-loop twins (stage code | 64, single.cuh ONE_LOOP) of the tuned configs:
 # the single kernel instantiates its tile loop per direction and once more for
